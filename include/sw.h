@@ -1,0 +1,185 @@
+/*
+ * sw.h -- C ABI of the B200-native batched Smith-Waterman (affine / Gotoh)
+ * library.  Product code; shares nothing with oracle/.
+ *
+ * What a batch computes (sec. II-B1, and the affine
+ * gap state of PAPER.md:507 / 713-714; tie rules are DESIGN.md readings
+ * R5/R6 = SURVEY.md sec. 8(c) C-4/C-5):
+ *
+ *   For every pair p, query q = queries[q_offsets[p] .. q_offsets[p+1])
+ *   (matrix rows i) and reference r = refs[r_offsets[p] .. r_offsets[p+1])
+ *   (matrix columns j):
+ *     E[i][j] = max(E[i][j-1] + gap_extend, H[i][j-1] + gap_open)
+ *     F[i][j] = max(F[i-1][j] + gap_extend, H[i-1][j] + gap_open)
+ *     H[i][j] = max(0, H[i-1][j-1] + s(q_i, r_j), E[i][j], F[i][j])
+ *   with H = 0 and E = F = -inf on the borders.  A gap of length k scores
+ *   gap_open + (k-1)*gap_extend.
+ *     score = S = max H                      (forward pass)
+ *     (q_end, r_end) = lexicographically smallest (r_end, q_end) with H = S
+ *     (q_start, r_start) from the same recurrence on the reversed prefixes
+ *       reverse(q[0..q_end]) x reverse(r[0..r_end]): the lexicographically
+ *       smallest reversed (j', i') with H' = S (reverse pass, PAPER.md:153/165,
+ *       "two CUDA kernels" PAPER.md:230).
+ *   Coordinates are 0-based, inclusive, relative to each sequence.
+ *   S == 0 (including an empty sequence)      -> (0, -1, -1, -1, -1)
+ *   invalid pair (symbol outside the alphabet,
+ *   negative length, length > SW_MAX_SEQ_LEN)  -> (-1, -1, -1, -1, -1)
+ *
+ * Alphabets (reading R10): DNA = A C G T; protein = the 24 BLOSUM62
+ * symbols A R N D C Q E G H I L K M F P S T W Y V B Z X *; both
+ * case-insensitive.  Protein always uses the built-in NCBI BLOSUM62.
+ *
+ * Threading: one host thread and one stream per handle at a time; a handle
+ * is bound to the device given to sw_init.  No function prints, throws or
+ * exits; errors are status codes (text via sw_last_error_message).
+ */
+#ifndef SW_B200_H
+#define SW_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SW_ABI_VERSION 1
+
+/* Longest sequence (either role) the library aligns; longer pairs are
+ * per-pair errors.  Positions fit 16 bits in the packed argmax key. */
+#define SW_MAX_SEQ_LEN 65535
+
+typedef struct sw_context* sw_handle_t;
+
+typedef enum {
+    SW_OK = 0,
+    SW_ERR_INVALID_ARGUMENT = 1, /* null handle/pointer, n_pairs < 0, ...            */
+    SW_ERR_INVALID_SCORING = 2,  /* preconditions on sw_scoring_t violated          */
+    SW_ERR_CUDA = 3,             /* a CUDA runtime call failed (see last error msg) */
+    SW_ERR_OUT_OF_MEMORY = 4,    /* workspace allocation failed                     */
+    SW_ERR_WRONG_DEVICE = 5,     /* current device differs from the handle's        */
+    SW_ERR_BAD_PAIRS = 6,        /* sw_batch_status: >= 1 pair was invalid          */
+    SW_ERR_INTERNAL = 7          /* a device self-check failed (never expected)     */
+} sw_status_t;
+
+typedef enum { SW_ALPHABET_DNA = 0, SW_ALPHABET_PROTEIN = 1 } sw_alphabet_t;
+
+/* Scoring (host struct, copied at the call).  Preconditions, checked
+ * synchronously (SW_ERR_INVALID_SCORING, nothing enqueued):
+ *   -32768 <= gap_open < 0  and  gap_open <= gap_extend <= 0
+ *   DNA: 0 < match <= 32767  and  -32768 <= mismatch < match
+ * (reading R3; "arbitrarily determined" scores). */
+typedef struct {
+    int32_t alphabet;   /* sw_alphabet_t                                       */
+    int32_t match;      /* DNA only: s(a, a)                                   */
+    int32_t mismatch;   /* DNA only: s(a, b), a != b                           */
+    int32_t gap_open;   /* score of the first residue of a gap (negative)      */
+    int32_t gap_extend; /* score of each further residue of the same gap       */
+} sw_scoring_t;
+
+/* Output arrays: caller-owned DEVICE memory, n_pairs int32 each, fully
+ * overwritten by sw_align_batch. */
+typedef struct {
+    int32_t* score;
+    int32_t* q_end;
+    int32_t* r_end;
+    int32_t* q_start;
+    int32_t* r_start;
+} sw_result_t;
+
+/* Create a handle bound to CUDA device `device`.  Allocates no large memory;
+ * the workspace grows on demand and is reused across calls. */
+sw_status_t sw_init(sw_handle_t* handle, int device);
+
+/*
+ * Align a batch (forward + reverse pass).
+ *   queries, refs     DEVICE uint8 ASCII bytes (CSR payloads)
+ *   q_offsets,
+ *   r_offsets         DEVICE int64, n_pairs + 1 entries each, non-decreasing;
+ *                     pair p uses [off[p], off[p+1]).  Offsets are relative to
+ *                     the payload pointers; off[0] need not be 0.
+ *   n_pairs           >= 0 (0 is a no-op)
+ *   scoring           HOST pointer, copied
+ *   out               HOST struct of DEVICE pointers (see sw_result_t)
+ *   stream            a cudaStream_t (NULL = legacy default stream)
+ * Work is enqueued on `stream`; inputs and outputs must stay untouched until
+ * it completes.  The call synchronises on `stream` twice (to read the payload
+ * extents q/r_offsets[0], [n_pairs] and the per-batch length statistics that
+ * size the workspace), so it returns after earlier work on `stream` is done
+ * but before this batch's kernels finish.  Per-pair errors do not fail the
+ * call: they appear as -1 sentinels and are counted by sw_batch_status.
+ */
+sw_status_t sw_align_batch(sw_handle_t h,
+                           const uint8_t* queries, const int64_t* q_offsets,
+                           const uint8_t* refs, const int64_t* r_offsets,
+                           int64_t n_pairs, const sw_scoring_t* scoring,
+                           const sw_result_t* out, void* stream);
+
+/*
+ * Same computation with HOST buffers (pinned memory recommended): copies the
+ * inputs to handle-owned device staging buffers, aligns, and copies the five
+ * result arrays to the HOST pointers in `out_host`.  Synchronous: returns
+ * after the results are on the host.  This is the end-to-end entry point.
+ */
+sw_status_t sw_align_batch_host(sw_handle_t h,
+                                const uint8_t* queries, const int64_t* q_offsets,
+                                const uint8_t* refs, const int64_t* r_offsets,
+                                int64_t n_pairs, const sw_scoring_t* scoring,
+                                const sw_result_t* out_host, void* stream);
+
+/* Synchronise the handle's last batch and report how many pairs were
+ * invalid.  Returns SW_OK, SW_ERR_BAD_PAIRS (count > 0) or SW_ERR_INTERNAL. */
+sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs);
+
+/* Synchronise outstanding work, release the workspace and the handle. */
+sw_status_t sw_free(sw_handle_t h);
+
+const char* sw_status_string(sw_status_t s);
+const char* sw_last_error_message(sw_handle_t h);
+
+/*
+ * Cell-count shard plan (host only, no device): cut pairs [0, n_pairs) into
+ * n_shards contiguous ranges of near-equal cost sum n_p*m_p (pairs with
+ * n_p*m_p == 0 cost 1).  q_offsets_host / r_offsets_host are HOST arrays of
+ * n_pairs + 1 entries; shard_begin receives n_shards + 1 indices with
+ * shard_begin[0] = 0 and shard_begin[n_shards] = n_pairs.
+ */
+sw_status_t sw_plan_shards(const int64_t* q_offsets_host, const int64_t* r_offsets_host,
+                           int64_t n_pairs, int32_t n_shards, int64_t* shard_begin);
+
+/* ---- instrumentation ------------------------------------------------ */
+
+/* Stage timers (CUDA events on the batch's stream).  Enable before a batch;
+ * read after it completes (sw_get_stage_ms synchronises on the last batch). */
+#define SW_STAGE_PACK 0      /* validation + ASCII -> codes + length stats       */
+#define SW_STAGE_SORT 1      /* forward length binning (radix sort)              */
+#define SW_STAGE_FWD 2       /* forward wavefront kernel(s)  <- dominant kernel  */
+#define SW_STAGE_MID 3       /* finish_fwd + reverse binning                     */
+#define SW_STAGE_REV 4       /* reverse wavefront kernel(s)                      */
+#define SW_STAGE_FINISH 5    /* finish_rev                                       */
+#define SW_STAGE_COUNT 6
+sw_status_t sw_enable_stage_timing(sw_handle_t h, int enable);
+sw_status_t sw_get_stage_ms(sw_handle_t h, float ms[SW_STAGE_COUNT]);
+
+/* Number of kernel launches the last batch enqueued (own kernels + CUB
+ * sort kernels counted separately). */
+sw_status_t sw_last_launch_count(sw_handle_t h, int32_t* own_kernels, int32_t* library_kernels);
+
+/* Forward/reverse cell counts of the last batch (after sw_batch_status or a
+ * stream sync): forward = sum n*m over valid pairs; padded = cells the
+ * wavefront actually swept (rows padded to the stripe, columns to the work
+ * item's longest reference, plus fill/drain). */
+sw_status_t sw_last_cell_counts(sw_handle_t h, int64_t* forward_cells, int64_t* swept_cells);
+
+/*
+ * DPX cell-update roofline probe: runs the minimal
+ * s16x2 Gotoh cell-pair mix (3 VIADDMNMX.S16x2 + 1 VIMNMX.S16x2 + 1
+ * VIADD.16x2 + 1/2 VIMNMX3.S16x2) on independent register chains on every
+ * SM for ~`milliseconds`, on `stream`.  Returns cell updates per second
+ * (2 per cell-pair step) in *cups.  Synchronous.
+ */
+sw_status_t sw_dpx_peak(int device, double milliseconds, double* cups, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SW_B200_H */

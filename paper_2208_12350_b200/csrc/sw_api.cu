@@ -1,0 +1,603 @@
+// sw_api.cu -- host side of the C ABI declared in include/sw.h: argument and
+// scoring validation, workspace management, the launch sequence
+//   pack -> sort -> forward wavefront -> finish_fwd -> sort -> reverse
+//   wavefront -> finish_rev
+// and the instrumentation entry points.  No exceptions cross the ABI.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sw.h"
+#include "sw_common.cuh"
+#include "sw_pack.cuh"
+#include "sw_wavefront.cuh"
+#include "sw_finish.cuh"
+
+using namespace swb;
+
+namespace {
+
+// Kernel geometry of this build: 16-lane segments, 10 rows
+// per lane -> 160-row stripes (one stripe covers the ADEPT-shaped 150 bp reads).
+constexpr int W16 = 16, K16 = 10;
+constexpr int W32 = 16, K32 = 10;
+constexpr int WARPS_PER_BLOCK = 4;
+constexpr int THREADS = WARPS_PER_BLOCK * 32;
+using G16 = Geometry<W16, K16, TS16>;
+using G32 = Geometry<W32, K32, TS32>;
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;  // elements
+};
+
+}  // namespace
+
+struct sw_context {
+    int device = 0;
+    int sm_count = 0;
+    int occ_s16_fwd = 1, occ_s16_rev = 1, occ_s32_fwd = 1, occ_s32_rev = 1;
+    int max_occ_cached_nc = -1;
+    cudaStream_t last_stream = nullptr;
+    bool have_last = false;
+    std::string err;
+
+    // per-pair
+    DevBuf<int32_t> nlen, mlen, nlen_rev, mlen_rev, target, iota, order, order_rev;
+    DevBuf<int64_t> rpos;
+    DevBuf<uint8_t> flags;
+    DevBuf<uint32_t> key, key_sorted;
+    DevBuf<unsigned long long> keys_fwd, keys_rev;
+    // codes
+    DevBuf<uint8_t> qcode, qrev, rcode, rrev;
+    // misc
+    DevBuf<uint8_t> cub_temp, scratch;
+    BatchStats* d_stats = nullptr;
+    BatchStats* h_stats = nullptr;
+    int64_t* h_ext = nullptr;
+    int32_t* d_counters = nullptr;  // 4 item counters
+    uint32_t* d_sink = nullptr;
+    // host-buffer entry point staging
+    DevBuf<uint8_t> st_q, st_r;
+    DevBuf<int64_t> st_qo, st_ro;
+    DevBuf<int32_t> st_out;
+
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    bool ev_valid = false;
+    int32_t own_launches = 0, lib_launches = 0;
+};
+
+namespace {
+
+sw_status_t fail(sw_context* h, sw_status_t st, const std::string& msg) {
+    if (h) h->err = msg;
+    return st;
+}
+
+sw_status_t cuda_fail(sw_context* h, cudaError_t e, const char* what) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    if (h) h->err = m;
+    return e == cudaErrorMemoryAllocation ? SW_ERR_OUT_OF_MEMORY : SW_ERR_CUDA;
+}
+
+#define SW_CUDA(h, call)                                          \
+    do {                                                          \
+        cudaError_t _e = (call);                                  \
+        if (_e != cudaSuccess) return cuda_fail((h), _e, #call);  \
+    } while (0)
+
+template <class T>
+sw_status_t ensure(sw_context* h, DevBuf<T>& b, size_t n) {
+    if (n == 0) n = 1;
+    if (b.cap >= n) return SW_OK;
+    size_t cap = std::max(n, (size_t)(b.cap * 5 / 4));
+    if (b.p) {
+        cudaError_t e = cudaFree(b.p);
+        b.p = nullptr; b.cap = 0;
+        if (e != cudaSuccess) return cuda_fail(h, e, "cudaFree");
+    }
+    cudaError_t e = cudaMalloc(&b.p, cap * sizeof(T));
+    if (e != cudaSuccess) {
+        // retry exact size
+        cap = n;
+        e = cudaMalloc(&b.p, cap * sizeof(T));
+        if (e != cudaSuccess) { b.p = nullptr; return cuda_fail(h, e, "cudaMalloc(workspace)"); }
+    }
+    b.cap = cap;
+    return SW_OK;
+}
+
+template <class T>
+void release(DevBuf<T>& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr; b.cap = 0;
+}
+
+// Scoring preconditions (reading R3) and the s16x2 routing condition.
+sw_status_t check_scoring(sw_context* h, const sw_scoring_t* s, Scoring& sc, bool& s16_ok) {
+    if (!s) return fail(h, SW_ERR_INVALID_ARGUMENT, "scoring is NULL");
+    if (s->alphabet != SW_ALPHABET_DNA && s->alphabet != SW_ALPHABET_PROTEIN)
+        return fail(h, SW_ERR_INVALID_SCORING, "unknown alphabet");
+    if (!(s->gap_open < 0) || s->gap_open < -32768)
+        return fail(h, SW_ERR_INVALID_SCORING, "gap_open must be in [-32768, 0)");
+    if (!(s->gap_open <= s->gap_extend && s->gap_extend <= 0))
+        return fail(h, SW_ERR_INVALID_SCORING, "need gap_open <= gap_extend <= 0");
+    int smax, smin;
+    if (s->alphabet == SW_ALPHABET_DNA) {
+        if (!(s->match > 0) || s->match > 32767) return fail(h, SW_ERR_INVALID_SCORING, "match must be in (0, 32767]");
+        if (!(s->mismatch < s->match) || s->mismatch < -32768)
+            return fail(h, SW_ERR_INVALID_SCORING, "mismatch must be in [-32768, match)");
+        smax = s->match; smin = std::min(s->mismatch, s->match);
+    } else {
+        smax = BLOSUM62_MAX; smin = BLOSUM62_MIN;
+    }
+    sc.alphabet = s->alphabet;
+    sc.match = s->match;
+    sc.mismatch = s->mismatch;
+    sc.gap_open = s->gap_open;
+    sc.gap_extend = s->gap_extend;
+    sc.nc = s->alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN;
+    sc.max_sigma = smax;
+    // s16x2 path: int8 profile of (s - o) in [-127, 127], gap values whose
+    // additions stay inside int16 (values live in [o + e, 32000]).
+    s16_ok = (smax - s->gap_open <= 127) && (smin - s->gap_open >= -127) &&
+             s->gap_open >= -8000 && s->gap_extend >= -8000;
+    return SW_OK;
+}
+
+template <class K>
+void set_smem_attr(K kernel, int bytes) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int occupancy_blocks(const void* kernel, int smem) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, THREADS, smem) != cudaSuccess) nb = 1;
+    return std::max(nb, 1);
+}
+
+struct Launch {
+    int blocks = 0;
+    int smem = 0;
+};
+
+template <class G>
+Launch plan_wave(const sw_context* h, const void* kernel, int nc, int64_t n_path) {
+    Launch l;
+    l.smem = WARPS_PER_BLOCK * G::warp_smem(nc);
+    const int64_t items = (n_path + G::SLOTS - 1) / G::SLOTS;
+    const int64_t need = (items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
+    const int64_t maxb = (int64_t)h->sm_count * occupancy_blocks(kernel, l.smem);
+    l.blocks = (int)std::max<int64_t>(0, std::min(need, maxb));
+    return l;
+}
+
+// The batch pipeline on device pointers.  host_ext (optional) = {q0, qN, r0, rN}.
+sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_off, const uint8_t* refs,
+                       const int64_t* r_off, int64_t n_pairs, const sw_scoring_t* scoring,
+                       const sw_result_t* out, cudaStream_t s, const int64_t* host_ext) {
+    int dev = -1;
+    SW_CUDA(h, cudaGetDevice(&dev));
+    if (dev != h->device) return fail(h, SW_ERR_WRONG_DEVICE, "current device differs from the handle's device");
+    Scoring sc;
+    bool s16_ok = false;
+    sw_status_t st = check_scoring(h, scoring, sc, s16_ok);
+    if (st != SW_OK) return st;
+    if (n_pairs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs < 0");
+    if (n_pairs > 0x7ffffff0LL) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs exceeds 2^31 - 16");
+    h->own_launches = 0;
+    h->lib_launches = 0;
+    h->ev_valid = false;
+    if (n_pairs == 0) return SW_OK;
+    if (!queries || !q_off || !refs || !r_off || !out || !out->score || !out->q_end || !out->r_end ||
+        !out->q_start || !out->r_start)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+    h->last_stream = s;
+    h->have_last = true;
+
+    // 1. payload extents
+    int64_t ext[4];
+    if (host_ext) {
+        std::memcpy(ext, host_ext, sizeof(ext));
+    } else {
+        SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 0, q_off, 8, cudaMemcpyDeviceToHost, s));
+        SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 1, q_off + n_pairs, 8, cudaMemcpyDeviceToHost, s));
+        SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 2, r_off, 8, cudaMemcpyDeviceToHost, s));
+        SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 3, r_off + n_pairs, 8, cudaMemcpyDeviceToHost, s));
+        SW_CUDA(h, cudaStreamSynchronize(s));
+        std::memcpy(ext, h->h_ext, sizeof(ext));
+    }
+    const int64_t q0 = ext[0], qN = ext[1], r0 = ext[2], rN = ext[3];
+    const size_t N = (size_t)n_pairs;
+    if (qN < q0 || rN < r0) {
+        fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, n_pairs);
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
+    }
+    const size_t tq = (size_t)(qN - q0), tr = (size_t)(rN - r0);
+    const size_t rbytes = tr + N * (PADL + PADR) + GUARD;
+
+    // 2. workspace
+#define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
+    ENS(nlen, N); ENS(mlen, N); ENS(nlen_rev, N); ENS(mlen_rev, N); ENS(target, N); ENS(iota, N);
+    ENS(order, N); ENS(order_rev, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
+    ENS(keys_fwd, N); ENS(keys_rev, N);
+    ENS(qcode, tq + 16); ENS(qrev, tq + 16); ENS(rcode, rbytes); ENS(rrev, rbytes);
+    {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p, h->key_sorted.p, h->iota.p, h->order.p,
+                                                  (int)N, 0, 32, s);
+        ENS(cub_temp, tb);
+    }
+
+    const int rows16 = G16::ROWS, rows32 = G32::ROWS;
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[0], s));
+
+    // 3. pack
+    SW_CUDA(h, cudaMemsetAsync(h->d_stats, 0, sizeof(BatchStats), s));
+    {
+        PackParams P;
+        P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.n_pairs = n_pairs;
+        P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN;
+        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma;
+        P.rows_s16 = rows16; P.rows_s32 = rows32;
+        P.qcode = h->qcode.p; P.rcode = h->rcode.p; P.rrev = h->rrev.p;
+        P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
+        P.iota = h->iota.p; P.stats = h->d_stats;
+        const int64_t warps = std::min<int64_t>(n_pairs, (int64_t)h->sm_count * 64);
+        const int blocks = (int)((warps * 32 + 255) / 256);
+        pack_kernel<<<blocks, 256, 0, s>>>(P);
+        SW_CUDA(h, cudaGetLastError());
+        ++h->own_launches;
+    }
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
+    // 4. statistics -> grids and scratch
+    SW_CUDA(h, cudaMemcpyAsync(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
+    SW_CUDA(h, cudaStreamSynchronize(s));
+    const BatchStats hs = *h->h_stats;
+    if (hs.malformed) {
+        fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, n_pairs);
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
+    }
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[2], s));
+
+    auto kf16 = wavefront_kernel<TS16, W16, K16, false>;
+    auto kr16 = wavefront_kernel<TS16, W16, K16, true>;
+    auto kf32 = wavefront_kernel<TS32, W32, K32, false>;
+    auto kr32 = wavefront_kernel<TS32, W32, K32, true>;
+    const Launch lf16 = plan_wave<G16>(h, (const void*)kf16, sc.nc, hs.n_s16);
+    const Launch lr16 = plan_wave<G16>(h, (const void*)kr16, sc.nc, hs.n_s16);
+    const Launch lf32 = plan_wave<G32>(h, (const void*)kf32, sc.nc, hs.n_s32);
+    const Launch lr32 = plan_wave<G32>(h, (const void*)kr32, sc.nc, hs.n_s32);
+
+    // stripe hand-off scratch: only if some query spans more than one stripe
+    int64_t seg16 = 0, seg32 = 0;
+    {
+        size_t need = 0;
+        const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16) * 8;
+        if (hs.n_s16 && hs.max_n > rows16) {
+            seg16 = row_bytes;
+            need = std::max(need, (size_t)std::max(lf16.blocks, lr16.blocks) * WARPS_PER_BLOCK * G16::SEGS * 2 * seg16);
+        }
+        if (hs.n_s32 && hs.max_n > rows32) {
+            seg32 = row_bytes;
+            need = std::max(need, (size_t)std::max(lf32.blocks, lr32.blocks) * WARPS_PER_BLOCK * G32::SEGS * 2 * seg32);
+        }
+        if (need) ENS(scratch, need);
+    }
+
+    // 5. forward binning (length-sorted, longest first)
+    SW_CUDA(h, cudaMemsetAsync(h->keys_fwd.p, 0, N * sizeof(unsigned long long), s));
+    {
+        size_t tb = h->cub_temp.cap;
+        SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp.p, tb, h->key.p, h->key_sorted.p, h->iota.p,
+                                                             h->order.p, (int)N, 0, 32, s));
+        ++h->lib_launches;
+    }
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[3], s));
+
+    // 6. forward wavefront
+    SW_CUDA(h, cudaMemsetAsync(h->d_counters, 0, 4 * sizeof(int32_t), s));
+    WaveParams W;
+    W.q_off = q_off; W.q0 = q0; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.sc = sc;
+    W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p;
+    W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &h->d_stats->swept_fwd;
+    if (lf16.blocks > 0) {
+        W.count = &h->d_stats->n_s16; W.first = nullptr; W.item_counter = h->d_counters + 0; W.scratch_seg_bytes = seg16;
+        kf16<<<lf16.blocks, THREADS, lf16.smem, s>>>(W);
+        SW_CUDA(h, cudaGetLastError());
+        ++h->own_launches;
+    }
+    if (lf32.blocks > 0) {
+        W.count = &h->d_stats->n_s32; W.first = &h->d_stats->n_s16; W.item_counter = h->d_counters + 1; W.scratch_seg_bytes = seg32;
+        kf32<<<lf32.blocks, THREADS, lf32.smem, s>>>(W);
+        SW_CUDA(h, cudaGetLastError());
+        ++h->own_launches;
+    }
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[4], s));
+
+    // 7. decode forward keys, prepare the reverse pass
+    FinishParams F;
+    F.n_pairs = n_pairs; F.flags = h->flags.p; F.keys_fwd = h->keys_fwd.p; F.keys_rev = h->keys_rev.p;
+    F.qcode = h->qcode.p; F.qrev = h->qrev.p; F.rcode = h->rcode.p; F.rrev = h->rrev.p;
+    F.q_off = q_off; F.q0 = q0; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
+    F.target = h->target.p; F.key_rev = h->key.p; F.iota = h->iota.p; F.rows_s16 = rows16; F.rows_s32 = rows32;
+    F.out = *out; F.stats = h->d_stats;
+    {
+        const int64_t warps = std::min<int64_t>(n_pairs, (int64_t)h->sm_count * 64);
+        finish_fwd_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(F);
+        SW_CUDA(h, cudaGetLastError());
+        ++h->own_launches;
+    }
+    SW_CUDA(h, cudaMemsetAsync(h->keys_rev.p, 0, N * sizeof(unsigned long long), s));
+    {
+        size_t tb = h->cub_temp.cap;
+        SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp.p, tb, h->key.p, h->key_sorted.p, h->iota.p,
+                                                             h->order_rev.p, (int)N, 0, 32, s));
+        ++h->lib_launches;
+    }
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[5], s));
+
+    // 8. reverse wavefront on the reversed prefixes
+    W.qcode = h->qrev.p; W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p;
+    W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &h->d_stats->swept_rev;
+    if (lr16.blocks > 0) {
+        W.count = &h->d_stats->n_rev_s16; W.first = nullptr; W.item_counter = h->d_counters + 2; W.scratch_seg_bytes = seg16;
+        kr16<<<lr16.blocks, THREADS, lr16.smem, s>>>(W);
+        SW_CUDA(h, cudaGetLastError());
+        ++h->own_launches;
+    }
+    if (lr32.blocks > 0) {
+        W.count = &h->d_stats->n_rev_s32; W.first = &h->d_stats->n_rev_s16; W.item_counter = h->d_counters + 3; W.scratch_seg_bytes = seg32;
+        kr32<<<lr32.blocks, THREADS, lr32.smem, s>>>(W);
+        SW_CUDA(h, cudaGetLastError());
+        ++h->own_launches;
+    }
+    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[6], s));
+
+    // 9. starts
+    finish_rev_kernel<<<(int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 16), 256, 0, s>>>(F);
+    SW_CUDA(h, cudaGetLastError());
+    ++h->own_launches;
+    if (h->timing) {
+        SW_CUDA(h, cudaEventRecord(h->ev[7], s));
+        h->ev_valid = true;
+    }
+    return SW_OK;
+#undef ENS
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sw_status_string(sw_status_t s) {
+    switch (s) {
+        case SW_OK: return "SW_OK";
+        case SW_ERR_INVALID_ARGUMENT: return "SW_ERR_INVALID_ARGUMENT";
+        case SW_ERR_INVALID_SCORING: return "SW_ERR_INVALID_SCORING";
+        case SW_ERR_CUDA: return "SW_ERR_CUDA";
+        case SW_ERR_OUT_OF_MEMORY: return "SW_ERR_OUT_OF_MEMORY";
+        case SW_ERR_WRONG_DEVICE: return "SW_ERR_WRONG_DEVICE";
+        case SW_ERR_BAD_PAIRS: return "SW_ERR_BAD_PAIRS";
+        case SW_ERR_INTERNAL: return "SW_ERR_INTERNAL";
+    }
+    return "SW_ERR_UNKNOWN";
+}
+
+const char* sw_last_error_message(sw_handle_t h) { return h ? h->err.c_str() : "null handle"; }
+
+sw_status_t sw_init(sw_handle_t* handle, int device) {
+    if (!handle) return SW_ERR_INVALID_ARGUMENT;
+    *handle = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) return SW_ERR_CUDA;
+    if (device < 0 || device >= n) return SW_ERR_INVALID_ARGUMENT;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return SW_ERR_CUDA;
+    if (cur != device) return SW_ERR_WRONG_DEVICE;
+    sw_context* h = new (std::nothrow) sw_context();
+    if (!h) return SW_ERR_OUT_OF_MEMORY;
+    h->device = device;
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) { delete h; return SW_ERR_CUDA; }
+    h->sm_count = p.multiProcessorCount;
+    // opt in to large dynamic shared memory (protein profiles)
+    const int big = 200 * 1024;
+    set_smem_attr(wavefront_kernel<TS16, W16, K16, false>, big);
+    set_smem_attr(wavefront_kernel<TS16, W16, K16, true>, big);
+    set_smem_attr(wavefront_kernel<TS32, W32, K32, false>, big);
+    set_smem_attr(wavefront_kernel<TS32, W32, K32, true>, big);
+    if (cudaMalloc(&h->d_stats, sizeof(BatchStats)) != cudaSuccess ||
+        cudaMallocHost(&h->h_stats, sizeof(BatchStats)) != cudaSuccess ||
+        cudaMallocHost(&h->h_ext, 4 * sizeof(int64_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_counters, 4 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess) {
+        sw_free(h);
+        return SW_ERR_OUT_OF_MEMORY;
+    }
+    cudaMemset(h->d_stats, 0, sizeof(BatchStats));
+    for (auto& ev : h->ev) {
+        if (cudaEventCreate(&ev) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
+    }
+    *handle = h;
+    return SW_OK;
+}
+
+sw_status_t sw_align_batch(sw_handle_t h, const uint8_t* queries, const int64_t* q_offsets, const uint8_t* refs,
+                           const int64_t* r_offsets, int64_t n_pairs, const sw_scoring_t* scoring,
+                           const sw_result_t* out, void* stream) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    return align_impl(h, queries, q_offsets, refs, r_offsets, n_pairs, scoring, out, (cudaStream_t)stream, nullptr);
+}
+
+sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int64_t* q_offsets, const uint8_t* refs,
+                                const int64_t* r_offsets, int64_t n_pairs, const sw_scoring_t* scoring,
+                                const sw_result_t* out_host, void* stream) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (n_pairs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs < 0");
+    if (n_pairs == 0) return SW_OK;
+    if (!queries || !q_offsets || !refs || !r_offsets || !out_host)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ext[4] = {q_offsets[0], q_offsets[n_pairs], r_offsets[0], r_offsets[n_pairs]};
+    if (ext[1] < ext[0] || ext[3] < ext[2]) return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
+    const size_t N = (size_t)n_pairs;
+    const size_t tq = (size_t)(ext[1] - ext[0]), tr = (size_t)(ext[3] - ext[2]);
+#define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
+    ENS(st_q, tq + 1); ENS(st_r, tr + 1); ENS(st_qo, N + 1); ENS(st_ro, N + 1); ENS(st_out, 5 * N);
+#undef ENS
+    // device copies keep the caller's offsets; payload pointer is shifted so offsets stay valid
+    SW_CUDA(h, cudaMemcpyAsync(h->st_q.p, queries + ext[0], tq, cudaMemcpyHostToDevice, s));
+    SW_CUDA(h, cudaMemcpyAsync(h->st_r.p, refs + ext[2], tr, cudaMemcpyHostToDevice, s));
+    SW_CUDA(h, cudaMemcpyAsync(h->st_qo.p, q_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, s));
+    SW_CUDA(h, cudaMemcpyAsync(h->st_ro.p, r_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, s));
+    sw_result_t dout;
+    dout.score = h->st_out.p; dout.q_end = h->st_out.p + N; dout.r_end = h->st_out.p + 2 * N;
+    dout.q_start = h->st_out.p + 3 * N; dout.r_start = h->st_out.p + 4 * N;
+    sw_status_t st = align_impl(h, h->st_q.p - ext[0], h->st_qo.p, h->st_r.p - ext[2], h->st_ro.p, n_pairs, scoring,
+                                &dout, s, ext);
+    if (st != SW_OK && st != SW_ERR_INVALID_ARGUMENT) return st;
+    int32_t* dst[5] = {out_host->score, out_host->q_end, out_host->r_end, out_host->q_start, out_host->r_start};
+    for (int k = 0; k < 5; ++k)
+        if (dst[k]) SW_CUDA(h, cudaMemcpyAsync(dst[k], h->st_out.p + k * N, N * 4, cudaMemcpyDeviceToHost, s));
+    SW_CUDA(h, cudaStreamSynchronize(s));
+    return st;
+}
+
+sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (n_bad_pairs) *n_bad_pairs = 0;
+    if (!h->have_last) return SW_OK;
+    SW_CUDA(h, cudaStreamSynchronize(h->last_stream));
+    SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
+    if (n_bad_pairs) *n_bad_pairs = h->h_stats->n_bad;
+    if (h->h_stats->internal_err) return fail(h, SW_ERR_INTERNAL, "reverse-pass self-check failed");
+    if (h->h_stats->malformed) {
+        if (n_bad_pairs) *n_bad_pairs = -1;
+        return SW_ERR_BAD_PAIRS;
+    }
+    return h->h_stats->n_bad ? SW_ERR_BAD_PAIRS : SW_OK;
+}
+
+sw_status_t sw_free(sw_handle_t h) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (h->have_last) cudaStreamSynchronize(h->last_stream);
+    cudaDeviceSynchronize();
+    release(h->nlen); release(h->mlen); release(h->nlen_rev); release(h->mlen_rev); release(h->target);
+    release(h->iota); release(h->order); release(h->order_rev); release(h->rpos); release(h->flags);
+    release(h->key); release(h->key_sorted); release(h->keys_fwd); release(h->keys_rev);
+    release(h->qcode); release(h->qrev); release(h->rcode); release(h->rrev); release(h->cub_temp);
+    release(h->scratch); release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
+    if (h->d_stats) cudaFree(h->d_stats);
+    if (h->h_stats) cudaFreeHost(h->h_stats);
+    if (h->h_ext) cudaFreeHost(h->h_ext);
+    if (h->d_counters) cudaFree(h->d_counters);
+    if (h->d_sink) cudaFree(h->d_sink);
+    for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
+    delete h;
+    return SW_OK;
+}
+
+sw_status_t sw_plan_shards(const int64_t* q_off, const int64_t* r_off, int64_t n_pairs, int32_t n_shards,
+                           int64_t* shard_begin) {
+    if (!q_off || !r_off || !shard_begin || n_pairs < 0 || n_shards < 1) return SW_ERR_INVALID_ARGUMENT;
+    std::vector<double> pre((size_t)n_pairs + 1, 0.0);
+    for (int64_t p = 0; p < n_pairs; ++p) {
+        const int64_t n = q_off[p + 1] - q_off[p], m = r_off[p + 1] - r_off[p];
+        const double c = (n > 0 && m > 0) ? (double)n * (double)m : 1.0;
+        pre[(size_t)p + 1] = pre[(size_t)p] + c;
+    }
+    const double total = pre[(size_t)n_pairs];
+    shard_begin[0] = 0;
+    int64_t p = 0;
+    for (int32_t k = 1; k < n_shards; ++k) {
+        const double goal = total * k / n_shards;
+        while (p < n_pairs && pre[(size_t)p + 1] <= goal) ++p;
+        // choose the cut (p or p+1) whose prefix is closer to the goal
+        int64_t cut = p;
+        if (p < n_pairs && (pre[(size_t)p + 1] - goal) < (goal - pre[(size_t)p])) cut = p + 1;
+        cut = std::max(cut, shard_begin[k - 1]);
+        shard_begin[k] = std::min(cut, n_pairs);
+    }
+    shard_begin[n_shards] = n_pairs;
+    return SW_OK;
+}
+
+sw_status_t sw_enable_stage_timing(sw_handle_t h, int enable) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    h->timing = enable != 0;
+    return SW_OK;
+}
+
+sw_status_t sw_get_stage_ms(sw_handle_t h, float ms[SW_STAGE_COUNT]) {
+    if (!h || !ms) return SW_ERR_INVALID_ARGUMENT;
+    for (int k = 0; k < SW_STAGE_COUNT; ++k) ms[k] = 0.f;
+    if (!h->ev_valid) return fail(h, SW_ERR_INVALID_ARGUMENT, "no timed batch");
+    SW_CUDA(h, cudaEventSynchronize(h->ev[7]));
+    // stage k spans events: pack 0-1, sort 2-3, fwd 3-4, mid 4-5, rev 5-6, finish 6-7
+    const int a[SW_STAGE_COUNT] = {0, 2, 3, 4, 5, 6};
+    const int b[SW_STAGE_COUNT] = {1, 3, 4, 5, 6, 7};
+    for (int k = 0; k < SW_STAGE_COUNT; ++k) SW_CUDA(h, cudaEventElapsedTime(&ms[k], h->ev[a[k]], h->ev[b[k]]));
+    return SW_OK;
+}
+
+sw_status_t sw_last_launch_count(sw_handle_t h, int32_t* own, int32_t* lib) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (own) *own = h->own_launches;
+    if (lib) *lib = h->lib_launches;
+    return SW_OK;
+}
+
+sw_status_t sw_last_cell_counts(sw_handle_t h, int64_t* fwd, int64_t* swept) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (h->have_last) SW_CUDA(h, cudaStreamSynchronize(h->last_stream));
+    SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
+    if (fwd) *fwd = (int64_t)h->h_stats->cells;
+    if (swept) *swept = (int64_t)h->h_stats->swept_fwd;
+    return SW_OK;
+}
+
+sw_status_t sw_dpx_peak(int device, double milliseconds, double* cups, void* stream) {
+    if (!cups) return SW_ERR_INVALID_ARGUMENT;
+    *cups = 0;
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess) return SW_ERR_CUDA;
+    if (cur != device) return SW_ERR_WRONG_DEVICE;
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return SW_ERR_CUDA;
+    cudaStream_t s = (cudaStream_t)stream;
+    uint32_t* sink = nullptr;
+    if (cudaMalloc(&sink, 1024 * 4) != cudaSuccess) return SW_ERR_OUT_OF_MEMORY;
+    const int blocks = p.multiProcessorCount * 8, threads = 256;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    int iters = 256;
+    float ms = 0.f;
+    sw_status_t st = SW_OK;
+    for (int round = 0; round < 8; ++round) {
+        cudaEventRecord(a, s);
+        dpx_peak_kernel<<<blocks, threads, 0, s>>>(sink, iters, 3u, 0xfffafffau, 0xffffffffu);
+        cudaEventRecord(b, s);
+        if (cudaEventSynchronize(b) != cudaSuccess) { st = SW_ERR_CUDA; break; }
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms >= 0.8 * milliseconds) break;
+        const double scale = std::min(64.0, std::max(2.0, milliseconds / std::max(ms, 0.01f)));
+        iters = (int)std::min(1e8, iters * scale);
+    }
+    if (st == SW_OK) {
+        const double cellpairs = (double)blocks * threads * iters * DPX_CHAINS;
+        *cups = 2.0 * cellpairs / (ms * 1e-3);
+    }
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    cudaFree(sink);
+    return st;
+}
+
+}  // extern "C"

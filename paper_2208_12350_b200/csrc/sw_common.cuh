@@ -1,0 +1,129 @@
+// sw_common.cuh -- constants, alphabet tables and the per-lane value traits of
+// the sm_100a Smith-Waterman path.  Product code: shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "sw.h"
+
+namespace swb {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+// Reference code layout: every reference gets PADL pad codes before it and
+// PADR after it, so the wavefront's fill/drain columns read pad codes without
+// bounds checks (the paper's "padding instead of boundary
+// checks" lesson, reused here).
+constexpr int PADL = 32;
+constexpr int PADR = 32;
+// Tail guard of the code buffers: a work item's shorter half keeps reading
+// (frozen, harmless) codes up to the item's longest reference + fill/drain.
+constexpr int64_t GUARD = SW_MAX_SEQ_LEN + 256;
+
+constexpr int NC_DNA = 5;        // A C G T + pad
+constexpr int NC_PROTEIN = 25;   // 24 BLOSUM62 symbols + pad
+constexpr uint8_t CODE_BAD = 0xff;
+
+// Forward/reverse work keys: [31] s16x2 path, [30] s32 path, [29:16] stripes, [15:0] m
+constexpr uint32_t KEY_S16 = 1u << 31;
+constexpr uint32_t KEY_S32 = 1u << 30;
+
+// per-pair flags
+constexpr uint8_t FLAG_BAD = 1;
+constexpr uint8_t FLAG_S16 = 2;
+
+// Product copy of NCBI BLOSUM62 (order ARNDCQEGHILKMFPSTWYVBZX*), R11.
+__constant__ int8_t c_blosum62[24][24] = {
+    { 4,-1,-2,-2, 0,-1,-1, 0,-2,-1,-1,-1,-1,-2,-1, 1, 0,-3,-2, 0,-2,-1, 0,-4},
+    {-1, 5, 0,-2,-3, 1, 0,-2, 0,-3,-2, 2,-1,-3,-2,-1,-1,-3,-2,-3,-1, 0,-1,-4},
+    {-2, 0, 6, 1,-3, 0, 0, 0, 1,-3,-3, 0,-2,-3,-2, 1, 0,-4,-2,-3, 3, 0,-1,-4},
+    {-2,-2, 1, 6,-3, 0, 2,-1,-1,-3,-4,-1,-3,-3,-1, 0,-1,-4,-3,-3, 4, 1,-1,-4},
+    { 0,-3,-3,-3, 9,-3,-4,-3,-3,-1,-1,-3,-1,-2,-3,-1,-1,-2,-2,-1,-3,-3,-2,-4},
+    {-1, 1, 0, 0,-3, 5, 2,-2, 0,-3,-2, 1, 0,-3,-1, 0,-1,-2,-1,-2, 0, 3,-1,-4},
+    {-1, 0, 0, 2,-4, 2, 5,-2, 0,-3,-3, 1,-2,-3,-1, 0,-1,-3,-2,-2, 1, 4,-1,-4},
+    { 0,-2, 0,-1,-3,-2,-2, 6,-2,-4,-4,-2,-3,-3,-2, 0,-2,-2,-3,-3,-1,-2,-1,-4},
+    {-2, 0, 1,-1,-3, 0, 0,-2, 8,-3,-3,-1,-2,-1,-2,-1,-2,-2, 2,-3, 0, 0,-1,-4},
+    {-1,-3,-3,-3,-1,-3,-3,-4,-3, 4, 2,-3, 1, 0,-3,-2,-1,-3,-1, 3,-3,-3,-1,-4},
+    {-1,-2,-3,-4,-1,-2,-3,-4,-3, 2, 4,-2, 2, 0,-3,-2,-1,-2,-1, 1,-4,-3,-1,-4},
+    {-1, 2, 0,-1,-3, 1, 1,-2,-1,-3,-2, 5,-1,-3,-1, 0,-1,-3,-2,-2, 0, 1,-1,-4},
+    {-1,-1,-2,-3,-1, 0,-2,-3,-2, 1, 2,-1, 5, 0,-2,-1,-1,-1,-1, 1,-3,-1,-1,-4},
+    {-2,-3,-3,-3,-2,-3,-3,-3,-1, 0, 0,-3, 0, 6,-4,-2,-2, 1, 3,-1,-3,-3,-1,-4},
+    {-1,-2,-2,-1,-3,-1,-1,-2,-2,-3,-3,-1,-2,-4, 7,-1,-1,-4,-3,-2,-2,-1,-2,-4},
+    { 1,-1, 1, 0,-1, 0, 0, 0,-1,-2,-2, 0,-1,-2,-1, 4, 1,-3,-2,-2, 0, 0, 0,-4},
+    { 0,-1, 0,-1,-1,-1,-1,-2,-2,-1,-1,-1,-1,-2,-1, 1, 5,-2,-2, 0,-1,-1, 0,-4},
+    {-3,-3,-4,-4,-2,-2,-3,-2,-2,-3,-2,-3,-1, 1,-4,-3,-2,11, 2,-3,-4,-3,-2,-4},
+    {-2,-2,-2,-3,-2,-1,-2,-3, 2,-1,-1,-2,-1, 3,-3,-2,-2, 2, 7,-1,-3,-2,-1,-4},
+    { 0,-3,-3,-3,-1,-2,-2,-3,-3, 3, 1,-2, 1,-1,-2,-2, 0,-3,-1, 4,-3,-2,-1,-4},
+    {-2,-1, 3, 4,-3, 0, 1,-1, 0,-3,-4, 0,-3,-3,-2, 0,-1,-4,-3,-3, 4, 1,-1,-4},
+    {-1, 0, 0, 1,-3, 3, 4,-2, 0,-3,-3, 1,-1,-3,-1, 0,-1,-3,-2,-2, 1, 4,-1,-4},
+    { 0,-1,-1,-1,-2,-1,-1,-1,-1,-1,-1,-1,-1,-1,-2, 0, 0,-2,-1,-1,-1,-1,-1,-4},
+    {-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4,-4, 1},
+};
+
+// Host-side max / min of BLOSUM62 (for routing decisions).
+constexpr int BLOSUM62_MAX = 11;
+constexpr int BLOSUM62_MIN = -4;
+
+struct Scoring {
+    int alphabet;
+    int match, mismatch;
+    int gap_open, gap_extend;
+    int nc;        // codes incl. pad
+    int max_sigma; // largest s(a,b)
+};
+
+__device__ __forceinline__ int sigma_of(const Scoring& sc, int a, int b) {
+    if (sc.alphabet == SW_ALPHABET_DNA) return a == b ? sc.match : sc.mismatch;
+    return c_blosum62[a][b];
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+    return d;
+}
+
+// ---------------------------------------------------------------------------
+// Per-lane value traits.  S16x2: every 32-bit register carries the same cell
+// of TWO different pairs (low / high 16-bit half), so one DPX instruction
+// advances two alignments.  S32: one pair per lane, int32 values (routing
+// fallback for scorings / lengths that are not int16-safe).
+// ---------------------------------------------------------------------------
+struct TS16 {
+    using V = uint32_t;
+    static constexpr int NH = 2;
+    static __device__ __forceinline__ V splat(int x) { return (uint32_t)(x & 0xffff) * 0x10001u; }
+    static __device__ __forceinline__ V add(V a, V b) { return __vadd2(a, b); }
+    // max(a + b, c)
+    static __device__ __forceinline__ V addmax(V a, V b, V c) { return __viaddmax_s16x2(a, b, c); }
+    static __device__ __forceinline__ V max_relu(V a, V b) { return __vimax_s16x2_relu(a, b); }
+    static __device__ __forceinline__ V max3(V a, V b, V c) { return __vimax3_s16x2_relu(a, b, c); }
+    static __device__ __forceinline__ V max2(V a, V b) { return __vimax_s16x2_relu(a, b); }
+    // per-half all-ones mask where a != b (a >= b per half guaranteed)
+    static __device__ __forceinline__ V changed_mask(V newv, V oldv) {
+        uint32_t d = newv - oldv;                       // per-half >= 0: no borrow
+        uint32_t nz = __vminu2(d, 0x00010001u);         // 0 or 1 per half
+        return nz * 0xffffu;
+    }
+    static __device__ __forceinline__ int get(V v, int h) { return (int)(int16_t)(uint16_t)(v >> (16 * h)); }
+    static __device__ __forceinline__ V set(V v, int h, int x) {
+        return h ? ((v & 0x0000ffffu) | ((uint32_t)(x & 0xffff) << 16)) : ((v & 0xffff0000u) | (uint32_t)(x & 0xffff));
+    }
+    static constexpr int FROZEN = 0x7fff;
+};
+
+struct TS32 {
+    using V = uint32_t;  // holds int32 bits
+    static constexpr int NH = 1;
+    static __device__ __forceinline__ V splat(int x) { return (uint32_t)x; }
+    static __device__ __forceinline__ V add(V a, V b) { return (uint32_t)((int)a + (int)b); }
+    static __device__ __forceinline__ V addmax(V a, V b, V c) { return (uint32_t)__viaddmax_s32((int)a, (int)b, (int)c); }
+    static __device__ __forceinline__ V max_relu(V a, V b) { return (uint32_t)__vimax_s32_relu((int)a, (int)b); }
+    static __device__ __forceinline__ V max3(V a, V b, V c) { return (uint32_t)__vimax3_s32_relu((int)a, (int)b, (int)c); }
+    static __device__ __forceinline__ V max2(V a, V b) { return (uint32_t)__vimax_s32_relu((int)a, (int)b); }
+    static __device__ __forceinline__ V changed_mask(V newv, V oldv) { return newv != oldv ? 0xffffffffu : 0u; }
+    static __device__ __forceinline__ int get(V v, int) { return (int)v; }
+    static __device__ __forceinline__ V set(V, int, int x) { return (uint32_t)x; }
+    static constexpr int FROZEN = 0x7fffffff;
+};
+
+}  // namespace swb

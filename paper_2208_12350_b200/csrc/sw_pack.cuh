@@ -1,0 +1,165 @@
+// sw_pack.cuh -- step a1 of SURVEY.md sec. 8(a): validation, ASCII -> codes,
+// per-pair lengths/flags/work keys and batch statistics, in one pass.
+#pragma once
+#include "sw_common.cuh"
+
+namespace swb {
+
+// Batch statistics written by the pack / finish kernels (device), read back
+// by the host once per batch to size grids and the stripe scratch.
+struct BatchStats {
+    int32_t n_bad;          // invalid pairs
+    int32_t n_s16;          // valid, non-trivial pairs routed to the s16x2 path
+    int32_t n_s32;          // ... routed to the s32 path
+    int32_t max_n;          // longest valid query
+    int32_t max_m;          // longest valid reference
+    int32_t malformed;      // offsets decrease somewhere -> whole batch invalid
+    int32_t n_rev_s16;      // pairs with S > 0 on each path (reverse pass)
+    int32_t n_rev_s32;
+    int32_t internal_err;   // self-check failures (reverse max != forward S)
+    int32_t pad_;
+    unsigned long long cells;        // sum n*m over valid pairs
+    unsigned long long swept_fwd;    // cells swept by the forward wavefront (incl. padding)
+    unsigned long long swept_rev;    // cells swept by the reverse wavefront
+};
+
+struct PackParams {
+    const uint8_t* queries;
+    const int64_t* q_off;
+    const uint8_t* refs;
+    const int64_t* r_off;
+    int64_t n_pairs;
+    int64_t q0, qN, r0, rN;      // payload extents (host-read)
+    int alphabet;
+    int s16_ok;                  // scoring fits the s16x2 path (int8 profile, int16 range)
+    int max_sigma;
+    int rows_s16, rows_s32;      // rows per stripe of each path
+    uint8_t* qcode;              // [qN - q0]
+    uint8_t* rcode;              // padded layout
+    uint8_t* rrev;               // padded layout (pads only here)
+    int32_t* nlen;
+    int32_t* mlen;
+    int64_t* rpos;
+    uint8_t* flags;
+    uint32_t* key;
+    int32_t* iota;
+    BatchStats* stats;
+};
+
+// ASCII -> code, case-insensitive; CODE_BAD outside the alphabet (reading R10).
+__device__ __forceinline__ uint8_t dna_code(uint8_t ch) {
+    ch &= 0xdf;  // upper-case letters (non-letters stay invalid below)
+    switch (ch) {
+        case 'A': return 0;
+        case 'C': return 1;
+        case 'G': return 2;
+        case 'T': return 3;
+        default: return CODE_BAD;
+    }
+}
+
+__device__ __forceinline__ uint8_t protein_code(uint8_t ch) {
+    if (ch == '*') return 23;
+    if (ch >= 'a' && ch <= 'z') ch -= 32;
+    // A R N D C Q E G H I L K M F P S T W Y V B Z X
+    switch (ch) {
+        case 'A': return 0;  case 'R': return 1;  case 'N': return 2;  case 'D': return 3;
+        case 'C': return 4;  case 'Q': return 5;  case 'E': return 6;  case 'G': return 7;
+        case 'H': return 8;  case 'I': return 9;  case 'L': return 10; case 'K': return 11;
+        case 'M': return 12; case 'F': return 13; case 'P': return 14; case 'S': return 15;
+        case 'T': return 16; case 'W': return 17; case 'Y': return 18; case 'V': return 19;
+        case 'B': return 20; case 'Z': return 21; case 'X': return 22;
+        default: return CODE_BAD;
+    }
+}
+
+__global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
+    __shared__ int s_bad, s_s16, s_s32, s_maxn, s_maxm, s_malformed;
+    __shared__ unsigned long long s_cells;
+    if (threadIdx.x == 0) { s_bad = s_s16 = s_s32 = s_maxn = s_maxm = s_malformed = 0; s_cells = 0; }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint8_t pad_code = (uint8_t)((P.alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN) - 1);
+    int l_bad = 0, l_s16 = 0, l_s32 = 0, l_maxn = 0, l_maxm = 0, l_malf = 0;
+    unsigned long long l_cells = 0;
+    for (int64_t p = gw; p < P.n_pairs; p += nw) {
+        const int64_t qa = P.q_off[p], qb = P.q_off[p + 1];
+        const int64_t ra = P.r_off[p], rb = P.r_off[p + 1];
+        const int64_t n = qb - qa, m = rb - ra;
+        bool in_range = qa >= P.q0 && qb <= P.qN && ra >= P.r0 && rb <= P.rN && n >= 0 && m >= 0;
+        if (n < 0 || m < 0) l_malf = 1;
+        bool bad = !in_range || n > SW_MAX_SEQ_LEN || m > SW_MAX_SEQ_LEN;
+        const int64_t rp = (ra - P.r0) + (p + 1) * PADL + p * PADR;
+        if (in_range) {
+            const int64_t qp = qa - P.q0;
+            for (int64_t i = lane; i < n; i += 32) {
+                uint8_t c = P.alphabet == SW_ALPHABET_DNA ? dna_code(P.queries[qa + i]) : protein_code(P.queries[qa + i]);
+                bad |= (c == CODE_BAD);
+                P.qcode[qp + i] = c;
+            }
+            for (int64_t j = lane; j < m; j += 32) {
+                uint8_t c = P.alphabet == SW_ALPHABET_DNA ? dna_code(P.refs[ra + j]) : protein_code(P.refs[ra + j]);
+                bad |= (c == CODE_BAD);
+                P.rcode[rp + j] = c;
+            }
+            // pads around the reference, in both the forward and the reverse buffer
+            for (int k = lane; k < PADL + PADR; k += 32) {
+                int64_t pos = k < PADL ? rp - PADL + k : rp + m + (k - PADL);
+                P.rcode[pos] = pad_code;
+                P.rrev[pos] = pad_code;
+            }
+        }
+        bad = __any_sync(FULL, bad);
+        if (lane == 0) {
+            uint32_t key = 0;
+            uint8_t fl = 0;
+            int nn = 0, mm = 0;
+            if (bad) {
+                fl = FLAG_BAD;
+                ++l_bad;
+            } else {
+                nn = (int)n; mm = (int)m;
+                const bool s16 = P.s16_ok && (int64_t)P.max_sigma * (int64_t)min(nn, mm) <= 32000;
+                fl = s16 ? FLAG_S16 : 0;
+                if (nn > 0 && mm > 0) {
+                    const int rows = s16 ? P.rows_s16 : P.rows_s32;
+                    const uint32_t stripes = min((nn + rows - 1) / rows, 0x3fff);
+                    key = (s16 ? KEY_S16 : KEY_S32) | (stripes << 16) | (uint32_t)mm;
+                    if (s16) ++l_s16; else ++l_s32;
+                    l_cells += (unsigned long long)nn * (unsigned long long)mm;
+                }
+                l_maxn = max(l_maxn, nn);
+                l_maxm = max(l_maxm, mm);
+            }
+            P.nlen[p] = nn;
+            P.mlen[p] = mm;
+            P.rpos[p] = rp;
+            P.flags[p] = fl;
+            P.key[p] = key;
+            P.iota[p] = (int32_t)p;
+        }
+    }
+    if (lane == 0) {
+        if (l_bad) atomicAdd(&s_bad, l_bad);
+        if (l_s16) atomicAdd(&s_s16, l_s16);
+        if (l_s32) atomicAdd(&s_s32, l_s32);
+        if (l_maxn) atomicMax(&s_maxn, l_maxn);
+        if (l_maxm) atomicMax(&s_maxm, l_maxm);
+        if (l_malf) atomicOr(&s_malformed, 1);
+        if (l_cells) atomicAdd(&s_cells, l_cells);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_bad) atomicAdd(&P.stats->n_bad, s_bad);
+        if (s_s16) atomicAdd(&P.stats->n_s16, s_s16);
+        if (s_s32) atomicAdd(&P.stats->n_s32, s_s32);
+        if (s_maxn) atomicMax(&P.stats->max_n, s_maxn);
+        if (s_maxm) atomicMax(&P.stats->max_m, s_maxm);
+        if (s_malformed) atomicOr(&P.stats->malformed, 1);
+        if (s_cells) atomicAdd(&P.stats->cells, s_cells);
+    }
+}
+
+}  // namespace swb

@@ -1,0 +1,374 @@
+// sw_wavefront.cuh -- steps a3 (forward: score + end) and a4 (reverse: start)
+// of SURVEY.md sec. 8(a): the anti-diagonal Gotoh wavefront on sm_100a.
+//
+// Recurrence (affine state PAPER.md:507/713-714), written
+// in the "HO" form the kernel keeps in registers (HO = H + gap_open):
+//   E[i][j]  = max(E[i][j-1] + e, HO[i][j-1])                 VIADDMNMX
+//   F[i][j]  = max(F[i-1][j] + e, HO[i-1][j])                 VIADDMNMX
+//   H[i][j]  = max(HO[i-1][j-1] + (s(q_i, r_j) - o),
+//                  max(E, F, 0))                               VIMNMX.RELU + VIADDMNMX
+//   HO[i][j] = H[i][j] + o                                     VIADD
+// which is the plain recurrence with E/F relu-clamped and -inf borders
+// replaced by gap_open (pin P13, reading R13).
+//
+// Layout (B200-first, not ADEPT's block-per-pair / thread-per-residue):
+// * a warp is split into 32/W segments of W lanes; a segment owns one (s32)
+//   or two (s16x2: low / high halves) pairs;
+// * lane L of a segment owns K consecutive query rows of the current stripe
+//   (W*K rows per stripe) and sweeps the reference column by column, skewed by
+//   one column per lane (anti-diagonal wavefront, PAPER.md:167-172 / Fig. 3);
+// * the row above (H and F of the lane's neighbour) arrives by one full-mask
+//   __shfl_up_sync per value per column -- no divergent shared-memory branch
+//   and no block barrier per anti-diagonal (lessons of PAPER.md:530-560);
+// * the substitution scores come from a per-stripe query profile in shared
+//   memory: (s - o) as int8 per (code, lane, row); two LDS.128 per column
+//   fetch all K rows of both halves, one PRMT per row interleaves and
+//   sign-extends them into an s16x2 operand;
+// * queries longer than W*K rows are processed as stripes; lane W-1 hands
+//   the stripe's bottom row (HO, F) to lane 0 of the next stripe through a
+//   per-warp global scratch row (L2-resident);
+// * the argmax keeps, per lane and half, the first column where the lane's
+//   running max improved (strict >) plus the HO values of that column, and
+//   emits one 64-bit key (S, -j, -i) per lane with atomicMax -- the lexmin
+//   (j, i) tie rule of reading R5 is associative, so lanes, halves and
+//   stripes merge in any order;
+// * REV mode runs the same kernel on the materialised reversed prefixes with
+//   target S: a lane that reaches S emits immediately and the item stops one
+//   segment-width after the first column holding S (reading R6).
+#pragma once
+#include "sw_common.cuh"
+#include "sw_pack.cuh"
+
+namespace swb {
+
+struct WaveParams {
+    const uint8_t* qcode;       // query codes (positions q_off[p] - q0)
+    const uint8_t* rcode;       // reference codes (padded positions rpos[p])
+    const int64_t* q_off;       // caller offsets (device)
+    int64_t q0;
+    const int64_t* rpos;
+    const int32_t* nlen;        // rows of each pair (forward: n, reverse: q_end+1)
+    const int32_t* mlen;        // columns (forward: m, reverse: r_end+1)
+    const int32_t* order;       // pair ids sorted by work key
+    const int32_t* count;       // device: pairs on this path
+    const int32_t* first;       // device: index of this path's first pair in order (nullptr = 0)
+    const int32_t* target;      // reverse: forward score per pair
+    unsigned long long* keys;   // per-pair atomicMax output
+    int32_t* item_counter;      // work queue head (zeroed before launch)
+    uint8_t* scratch;           // stripe hand-off rows
+    int64_t scratch_seg_bytes;  // bytes of one segment x parity buffer
+    unsigned long long* swept;  // cells swept (statistics)
+    Scoring sc;
+};
+
+template <int W, int K, class T>
+struct Geometry {
+    static constexpr int SEGS = 32 / W;
+    static constexpr int SLOTS = SEGS * T::NH;
+    static constexpr int ROWS = W * K;                       // rows per stripe
+    // profile bytes per (slot, code, lane): int8 x K (s16x2) or int32 x K (s32), 16 B aligned
+    static constexpr int PB = (T::NH == 2) ? 16 * ((K + 15) / 16) : 16 * ((4 * K + 15) / 16);
+    static constexpr int PWORDS = PB / 4;
+    static __host__ __device__ int prof_bytes(int nc) { return SLOTS * nc * W * PB; }
+    // shared memory per warp: profile + REV stop steps
+    static __host__ __device__ int warp_smem(int nc) { return prof_bytes(nc) + 16 * ((SLOTS * 4 + 15) / 16); }
+};
+
+template <class T, int K>
+struct LaneState {
+    uint32_t HO[K];   // H + o of the lane's rows at the previous column
+    uint32_t E[K];    // E of the lane's rows at the previous column
+    uint32_t SV[K];   // HO of the column where the lane's best last improved
+};
+
+template <class T, int W, int K, bool REV>
+__global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
+    using G = Geometry<W, K, T>;
+    constexpr int NH = T::NH;
+    constexpr int SLOTS = G::SLOTS;
+    constexpr int U = 4;  // column unroll
+    extern __shared__ __align__(16) uint8_t smem[];
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int seg = lane / W;
+    const int L = lane % W;
+    const int nc = P.sc.nc;
+    uint8_t* prof = smem + (size_t)warp * G::warp_smem(nc);
+    volatile int* stop = reinterpret_cast<volatile int*>(prof + G::prof_bytes(nc));
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+
+    const int n_path = *P.count;
+    const int first = P.first ? *P.first : 0;
+    const int items = (n_path + SLOTS - 1) / SLOTS;
+    const uint32_t o2 = T::splat(P.sc.gap_open);
+    const uint32_t e2 = T::splat(P.sc.gap_extend);
+    const int o = P.sc.gap_open;
+
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(P.item_counter, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= items) break;
+
+        // ---- slot descriptors (lane s < SLOTS holds slot s) ----
+        int s_pid = -1, s_n = 0, s_m = 0, s_tgt = 0;
+        int64_t s_rpos = 0, s_qpos = 0;
+        if (lane < SLOTS) {
+            const int idx = item * SLOTS + lane;
+            if (idx < n_path) {
+                s_pid = P.order[first + idx];
+                s_n = P.nlen[s_pid];
+                s_m = P.mlen[s_pid];
+                s_rpos = P.rpos[s_pid];
+                s_qpos = P.q_off[s_pid] - P.q0;
+                if (REV) s_tgt = P.target[s_pid];
+            }
+        }
+        int mmax = s_m, nmax = s_n;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+            mmax = max(mmax, __shfl_xor_sync(FULL, mmax, d));
+            nmax = max(nmax, __shfl_xor_sync(FULL, nmax, d));
+        }
+        const int ns = (nmax + G::ROWS - 1) / G::ROWS;
+
+        // this lane's halves
+        int h_pid[NH], h_m[NH], h_tgt[NH];
+        int64_t h_rpos[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            const int sl = seg * NH + h;
+            h_pid[h] = __shfl_sync(FULL, s_pid, sl);
+            h_m[h] = __shfl_sync(FULL, s_m, sl);
+            h_tgt[h] = __shfl_sync(FULL, s_tgt, sl);
+            h_rpos[h] = __shfl_sync(FULL, s_rpos, sl);
+            if (h_pid[h] < 0) h_rpos[h] = PADL;  // empty slot: read pad region at buffer start
+        }
+        const int T_steps = mmax + W - 1;
+        if (lane == 0) atomicAdd(P.swept, (unsigned long long)ns * G::ROWS * (unsigned long long)T_steps * SLOTS);
+
+        if (REV) {
+            __syncwarp();
+            if (lane < SLOTS) stop[lane] = 0x7fffffff;
+        }
+        for (int s = 0; s < ns; ++s) {
+            const int row0 = s * G::ROWS;
+            // ---- build the stripe's query profile: (s - o) per (slot, code, lane, row) ----
+            __syncwarp();
+            {
+                constexpr int COMBOS = SLOTS * W * G::PWORDS;
+                for (int cb = lane; cb < ((COMBOS + 31) / 32) * 32; cb += 32) {
+                    const int sl = (cb / (W * G::PWORDS)) % SLOTS;
+                    const int pid = __shfl_sync(FULL, s_pid, sl);
+                    const int n = __shfl_sync(FULL, s_n, sl);
+                    const int64_t qp = __shfl_sync(FULL, s_qpos, sl);
+                    if (cb >= COMBOS) continue;
+                    const int l = (cb / G::PWORDS) % W;
+                    const int w = cb % G::PWORDS;
+                    uint8_t* base = prof + (size_t)sl * nc * W * G::PB + (size_t)l * G::PB + w * 4;
+                    if (NH == 2) {
+                        int qc[4];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int r = w * 4 + b;
+                            const int i = row0 + l * K + r;
+                            qc[b] = (pid >= 0 && r < K && i < n) ? P.qcode[qp + i] : -1;
+                        }
+                        for (int c = 0; c < nc; ++c) {
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int b = 0; b < 4; ++b) {
+                                int v = -128;
+                                if (qc[b] >= 0 && c < nc - 1) v = sigma_of(P.sc, qc[b], c) - o;
+                                word |= (uint32_t)(v & 0xff) << (8 * b);
+                            }
+                            *reinterpret_cast<uint32_t*>(base + (size_t)c * W * G::PB) = word;
+                        }
+                    } else {
+                        const int r = w;
+                        const int i = row0 + l * K + r;
+                        const int qc = (pid >= 0 && r < K && i < n) ? P.qcode[qp + i] : -1;
+                        for (int c = 0; c < nc; ++c) {
+                            int v = -(1 << 29);
+                            if (qc >= 0 && c < nc - 1) v = sigma_of(P.sc, qc, c) - o;
+                            *reinterpret_cast<int32_t*>(base + (size_t)c * W * G::PB) = v;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+
+            // ---- per-stripe lane state ----
+            LaneState<T, K> st;
+#pragma unroll
+            for (int r = 0; r < K; ++r) { st.HO[r] = o2; st.E[r] = o2; st.SV[r] = 0; }
+            uint32_t best = 0, bestcol = 0;
+            uint32_t hoLast = o2, fLast = o2, prevUpHO = o2;
+            int ev[NH];
+            int next_ev = 0x7fffffff;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                ev[h] = (!REV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
+                next_ev = min(next_ev, ev[h]);
+            }
+            const bool from_scratch = s > 0;
+            const bool to_scratch = s + 1 < ns;
+            const uint2* scr_in = reinterpret_cast<const uint2*>(P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes);
+            uint2* scr_out = reinterpret_cast<uint2*>(P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
+            const uint8_t* prof_h[NH];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) prof_h[h] = prof + (size_t)(seg * NH + h) * nc * W * G::PB + (size_t)L * G::PB;
+            const size_t code_stride = (size_t)W * G::PB;
+
+            // prefetch of reference codes and boundary rows, one U-block ahead.  Codes are
+            // clamped to the profile: a finished (frozen) half keeps reading past its
+            // reference into bytes that may be stale or CODE_BAD.
+            uint8_t cd[U][NH];
+            uint2 bnd[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) cd[u][h] = (uint8_t)min((int)P.rcode[h_rpos[h] + (u - L)], nc - 1);
+                bnd[u] = (from_scratch && L == 0) ? __ldcg(scr_in + u) : make_uint2(o2, o2);
+            }
+
+            int T_end = T_steps;
+            if (REV) {
+                int te = 0;
+#pragma unroll
+                for (int sl = 0; sl < SLOTS; ++sl) {
+                    const int m_sl = __shfl_sync(FULL, s_m, sl);
+                    te = max(te, min(m_sl + W - 1, stop[sl]));
+                }
+                T_end = te;
+            }
+            for (int t0 = 0; t0 < T_end; t0 += U) {
+                uint8_t cdn[U][NH];
+                uint2 bndn[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) cdn[u][h] = (uint8_t)min((int)P.rcode[h_rpos[h] + (t0 + U + u - L)], nc - 1);
+                    bndn[u] = (from_scratch && L == 0) ? __ldcg(scr_in + t0 + U + u) : make_uint2(o2, o2);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int t = t0 + u;
+                    // profile words of this lane's column, both halves
+                    uint32_t pw[NH][G::PWORDS];
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        const uint4* src = reinterpret_cast<const uint4*>(prof_h[h] + cd[u][h] * code_stride);
+#pragma unroll
+                        for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
+                            uint4 v = src[q4];
+                            pw[h][q4 * 4 + 0] = v.x; pw[h][q4 * 4 + 1] = v.y;
+                            pw[h][q4 * 4 + 2] = v.z; pw[h][q4 * 4 + 3] = v.w;
+                        }
+                    }
+                    // row above: neighbour lane's last row (this column), or the stripe boundary
+                    uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W);
+                    uint32_t upF = __shfl_up_sync(FULL, fLast, 1, W);
+                    if (L == 0) { upHO = bnd[u].x; upF = bnd[u].y; }
+                    uint32_t hd = prevUpHO;
+                    prevUpHO = upHO;
+                    uint32_t F = upF, hu = upHO;
+                    uint32_t H[K];
+#pragma unroll
+                    for (int r = 0; r < K; ++r) {
+                        uint32_t sc;
+                        if (NH == 2) {
+                            constexpr uint32_t SEL[4] = {0xC480u, 0xD591u, 0xE6A2u, 0xF7B3u};
+                            sc = prmt(pw[0][r >> 2], pw[1][r >> 2], SEL[r & 3]);
+                        } else {
+                            sc = pw[0][r];
+                        }
+                        st.E[r] = T::addmax(st.E[r], e2, st.HO[r]);
+                        F = T::addmax(F, e2, hu);
+                        const uint32_t tt = T::max_relu(st.E[r], F);
+                        const uint32_t h = T::addmax(hd, sc, tt);
+                        hd = st.HO[r];
+                        st.HO[r] = T::add(h, o2);
+                        hu = st.HO[r];
+                        H[r] = h;
+                    }
+                    hoLast = st.HO[K - 1];
+                    fLast = F;
+                    // running max over the lane's rows (strict improvement -> record column)
+                    uint32_t nb = best;
+#pragma unroll
+                    for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
+                    if (K & 1) nb = T::max2(nb, H[K - 1]);
+                    if (nb != best) {
+                        const uint32_t mask = T::changed_mask(nb, best);
+#pragma unroll
+                        for (int r = 0; r < K; ++r) st.SV[r] = (st.SV[r] & ~mask) | (st.HO[r] & mask);
+                        bestcol = (bestcol & ~mask) | (T::splat(t - L) & mask);
+                        best = nb;
+                        if (REV) {
+#pragma unroll
+                            for (int h = 0; h < NH; ++h) {
+                                if (h_pid[h] >= 0 && T::get(mask, h) != 0 && T::get(best, h) == h_tgt[h]) {
+                                    int rr = 0;
+#pragma unroll
+                                    for (int r = K - 1; r >= 0; --r) if (T::get(st.SV[r], h) == h_tgt[h] + o) rr = r;
+                                    const int j = t - L;
+                                    const int i = row0 + L * K + rr;
+                                    const unsigned long long key = ((unsigned long long)(uint32_t)h_tgt[h] << 32) |
+                                        ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
+                                    atomicMax(P.keys + h_pid[h], key);
+                                    atomicMin((int*)stop + seg * NH + h, j + W);
+                                }
+                            }
+                        }
+                    }
+                    if (!REV && t == next_ev) {
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) {
+                            if (ev[h] == t) {
+                                const int b = T::get(best, h);
+                                if (b > 0) {
+                                    int rr = 0;
+#pragma unroll
+                                    for (int r = K - 1; r >= 0; --r) if (T::get(st.SV[r], h) == b + o) rr = r;
+                                    const int j = (NH == 2) ? (int)((bestcol >> (16 * h)) & 0xffff) : (int)bestcol;
+                                    const int i = row0 + L * K + rr;
+                                    const unsigned long long key = ((unsigned long long)(uint32_t)b << 32) |
+                                        ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
+                                    atomicMax(P.keys + h_pid[h], key);
+                                }
+                                best = T::set(best, h, T::FROZEN);
+                                ev[h] = 0x7fffffff;
+                            }
+                        }
+                        next_ev = ev[0];
+                        if (NH == 2) next_ev = min(next_ev, ev[NH - 1]);
+                    }
+                    if (to_scratch && L == W - 1) {
+                        const int c = t - (W - 1);
+                        if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) cd[u][h] = cdn[u][h];
+                    bnd[u] = bndn[u];
+                }
+                if (REV) {
+                    __syncwarp();
+                    int te = 0;
+#pragma unroll
+                    for (int sl = 0; sl < SLOTS; ++sl) {
+                        const int m_sl = __shfl_sync(FULL, s_m, sl);
+                        te = max(te, min(m_sl + W - 1, stop[sl]));
+                    }
+                    T_end = te;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace swb

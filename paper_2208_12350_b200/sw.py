@@ -1,0 +1,259 @@
+"""Thin ctypes binding of the C ABI in include/sw.h (argument marshalling only).
+
+Every step of the alignment runs in ``libsw_b200.so`` (sm_100a kernels).  There
+is no CPU fallback: if the library cannot be loaded, the calls raise.  The
+function names mirror the C ABI (``sw_init``, ``sw_align_batch``,
+``sw_align_batch_host``, ``sw_free``, ``sw_batch_status``, ``sw_plan_shards``,
+...); ``Aligner`` is a convenience wrapper over torch tensors (PyTorch is used
+only for device memory and streams).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import _build
+
+SW_OK = 0
+SW_ERR_INVALID_ARGUMENT = 1
+SW_ERR_INVALID_SCORING = 2
+SW_ERR_CUDA = 3
+SW_ERR_OUT_OF_MEMORY = 4
+SW_ERR_WRONG_DEVICE = 5
+SW_ERR_BAD_PAIRS = 6
+SW_ERR_INTERNAL = 7
+
+SW_ALPHABET_DNA = 0
+SW_ALPHABET_PROTEIN = 1
+SW_MAX_SEQ_LEN = 65535
+SW_STAGE_NAMES = ("pack", "sort", "fwd", "mid", "rev", "finish")
+
+EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_batch_status", "sw_free",
+            "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
+            "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_dpx_peak")
+
+
+class sw_scoring_t(ctypes.Structure):
+    _fields_ = [("alphabet", ctypes.c_int32), ("match", ctypes.c_int32), ("mismatch", ctypes.c_int32),
+                ("gap_open", ctypes.c_int32), ("gap_extend", ctypes.c_int32)]
+
+
+class sw_result_t(ctypes.Structure):
+    _fields_ = [("score", ctypes.c_void_p), ("q_end", ctypes.c_void_p), ("r_end", ctypes.c_void_p),
+                ("q_start", ctypes.c_void_p), ("r_start", ctypes.c_void_p)]
+
+
+class SWError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        super().__init__(f"{status_string(status)}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return _build.LIB
+
+
+def load(build_if_missing: bool = True):
+    """Load libsw_b200.so (building it with nvcc if absent).  Raises if unavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = _build.LIB
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise OSError(f"{path} not built (run __graft_entry__.build())")
+        _build.build()
+    lib = ctypes.CDLL(path)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32
+    sp = ctypes.POINTER(sw_scoring_t)
+    rp = ctypes.POINTER(sw_result_t)
+    lib.sw_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
+    lib.sw_align_batch.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
+    lib.sw_align_batch_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
+    lib.sw_batch_status.argtypes = [vp, ctypes.POINTER(i64)]
+    lib.sw_free.argtypes = [vp]
+    lib.sw_status_string.argtypes = [ctypes.c_int]
+    lib.sw_status_string.restype = ctypes.c_char_p
+    lib.sw_last_error_message.argtypes = [vp]
+    lib.sw_last_error_message.restype = ctypes.c_char_p
+    lib.sw_plan_shards.argtypes = [vp, vp, i64, i32, vp]
+    lib.sw_enable_stage_timing.argtypes = [vp, ctypes.c_int]
+    lib.sw_get_stage_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
+    lib.sw_last_launch_count.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.sw_last_cell_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.sw_dpx_peak.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]
+    for name in EXPORTED:
+        if name not in ("sw_status_string", "sw_last_error_message"):
+            getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def status_string(st: int) -> str:
+    try:
+        return load().sw_status_string(int(st)).decode()
+    except OSError:
+        return f"status {st}"
+
+
+def make_scoring(scoring: dict) -> sw_scoring_t:
+    a = scoring.get("alphabet", "dna")
+    a = {"dna": SW_ALPHABET_DNA, "protein": SW_ALPHABET_PROTEIN}[a] if isinstance(a, str) else int(a)
+    return sw_scoring_t(a, int(scoring.get("match", 0)), int(scoring.get("mismatch", 0)),
+                        int(scoring["gap_open"]), int(scoring["gap_extend"]))
+
+
+# ------------------------------------------------------------ C-ABI mirrors
+
+def sw_init(device: int) -> int:
+    lib = load()
+    h = ctypes.c_void_p()
+    st = lib.sw_init(ctypes.byref(h), int(device))
+    if st != SW_OK:
+        raise SWError(st, "sw_init")
+    return h.value
+
+
+def sw_free(handle: int) -> None:
+    st = load().sw_free(ctypes.c_void_p(handle))
+    if st != SW_OK:
+        raise SWError(st, "sw_free")
+
+
+def sw_last_error_message(handle: int) -> str:
+    return load().sw_last_error_message(ctypes.c_void_p(handle)).decode()
+
+
+def sw_align_batch(handle: int, queries, q_offsets, refs, r_offsets, n_pairs: int, scoring: dict, out: dict,
+                   stream: int = 0) -> int:
+    """Device pointers (ints) in, device pointers in ``out`` (dict of 5). Returns the status."""
+    lib = load()
+    sc = make_scoring(scoring)
+    res = sw_result_t(out["score"], out["q_end"], out["r_end"], out["q_start"], out["r_start"])
+    return lib.sw_align_batch(ctypes.c_void_p(handle), ctypes.c_void_p(queries), ctypes.c_void_p(q_offsets),
+                              ctypes.c_void_p(refs), ctypes.c_void_p(r_offsets), int(n_pairs), ctypes.byref(sc),
+                              ctypes.byref(res), ctypes.c_void_p(stream))
+
+
+def sw_align_batch_host(handle: int, queries, q_offsets, refs, r_offsets, n_pairs: int, scoring: dict, out: dict,
+                        stream: int = 0) -> int:
+    lib = load()
+    sc = make_scoring(scoring)
+    res = sw_result_t(out["score"], out["q_end"], out["r_end"], out["q_start"], out["r_start"])
+    return lib.sw_align_batch_host(ctypes.c_void_p(handle), ctypes.c_void_p(queries), ctypes.c_void_p(q_offsets),
+                                   ctypes.c_void_p(refs), ctypes.c_void_p(r_offsets), int(n_pairs),
+                                   ctypes.byref(sc), ctypes.byref(res), ctypes.c_void_p(stream))
+
+
+def sw_batch_status(handle: int) -> tuple[int, int]:
+    n = ctypes.c_int64(0)
+    st = load().sw_batch_status(ctypes.c_void_p(handle), ctypes.byref(n))
+    return st, n.value
+
+
+def sw_plan_shards(q_offsets: np.ndarray, r_offsets: np.ndarray, n_shards: int) -> np.ndarray:
+    """Host-only cell-count shard plan: n_shards + 1 contiguous cut indices."""
+    qo = np.ascontiguousarray(q_offsets, dtype=np.int64)
+    ro = np.ascontiguousarray(r_offsets, dtype=np.int64)
+    n = qo.size - 1
+    out = np.zeros(int(n_shards) + 1, dtype=np.int64)
+    st = load().sw_plan_shards(qo.ctypes.data, ro.ctypes.data, n, int(n_shards), out.ctypes.data)
+    if st != SW_OK:
+        raise SWError(st, "sw_plan_shards")
+    return out
+
+
+def sw_dpx_peak(device: int, milliseconds: float = 200.0, stream: int = 0) -> float:
+    cups = ctypes.c_double(0)
+    st = load().sw_dpx_peak(int(device), float(milliseconds), ctypes.byref(cups), ctypes.c_void_p(stream))
+    if st != SW_OK:
+        raise SWError(st, "sw_dpx_peak")
+    return cups.value
+
+
+# ------------------------------------------------------ torch convenience
+
+class Aligner:
+    """Owns one sw handle on one device; aligns batches held in torch tensors."""
+
+    def __init__(self, device: int = 0):
+        import torch
+        self.torch = torch
+        self.device = int(device)
+        torch.cuda.set_device(self.device)
+        self.handle = sw_init(self.device)
+
+    def close(self):
+        if self.handle:
+            sw_free(self.handle)
+            self.handle = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def to_device(self, batch):
+        t = self.torch
+        dev = f"cuda:{self.device}"
+        q = t.from_numpy(np.ascontiguousarray(batch.queries)).to(dev) if batch.queries.size else t.zeros(1, dtype=t.uint8, device=dev)
+        r = t.from_numpy(np.ascontiguousarray(batch.refs)).to(dev) if batch.refs.size else t.zeros(1, dtype=t.uint8, device=dev)
+        qo = t.from_numpy(np.ascontiguousarray(batch.q_offsets)).to(dev)
+        ro = t.from_numpy(np.ascontiguousarray(batch.r_offsets)).to(dev)
+        return q, qo, r, ro
+
+    def alloc_out(self, n: int):
+        t = self.torch
+        buf = t.empty((5, max(n, 1)), dtype=t.int32, device=f"cuda:{self.device}")
+        return buf
+
+    def align_tensors(self, q, qo, r, ro, scoring: dict, out=None, stream=None, check=True):
+        t = self.torch
+        n = qo.numel() - 1
+        if out is None:
+            out = self.alloc_out(n)
+        s = stream if stream is not None else t.cuda.current_stream(self.device)
+        ptrs = {k: out[i].data_ptr() for i, k in enumerate(("score", "q_end", "r_end", "q_start", "r_start"))}
+        st = sw_align_batch(self.handle, q.data_ptr(), qo.data_ptr(), r.data_ptr(), ro.data_ptr(), n, scoring, ptrs,
+                            s.cuda_stream)
+        if check and st != SW_OK:
+            raise SWError(st, sw_last_error_message(self.handle))
+        return out, st
+
+    def align(self, batch, check=True) -> dict:
+        """Align a synth.Batch; returns dict of five int32 numpy arrays."""
+        q, qo, r, ro = self.to_device(batch)
+        out, st = self.align_tensors(q, qo, r, ro, batch.scoring, check=check)
+        self.torch.cuda.synchronize(self.device)
+        n = batch.n_pairs
+        o = out[:, :n].cpu().numpy()
+        return {k: o[i] for i, k in enumerate(("score", "q_end", "r_end", "q_start", "r_start"))}
+
+    def batch_status(self):
+        return sw_batch_status(self.handle)
+
+    def stage_ms(self) -> dict:
+        arr = (ctypes.c_float * 6)()
+        st = load().sw_get_stage_ms(ctypes.c_void_p(self.handle), arr)
+        if st != SW_OK:
+            raise SWError(st, sw_last_error_message(self.handle))
+        return dict(zip(SW_STAGE_NAMES, list(arr)))
+
+    def enable_stage_timing(self, on: bool = True):
+        load().sw_enable_stage_timing(ctypes.c_void_p(self.handle), 1 if on else 0)
+
+    def launch_count(self):
+        a, b = ctypes.c_int32(0), ctypes.c_int32(0)
+        load().sw_last_launch_count(ctypes.c_void_p(self.handle), ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value
+
+    def cell_counts(self):
+        a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+        load().sw_last_cell_counts(ctypes.c_void_p(self.handle), ctypes.byref(a), ctypes.byref(b))
+        return a.value, b.value

@@ -1,0 +1,281 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle.
+
+Bar: every pair, all five fields, bit-exact.
+Inputs are the seeded synthetic batches of paper_2208_12350_b200.synth; the
+oracle is called only here, on the same bytes.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2208_12350_b200 import sw, synth
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("score", "q_end", "r_end", "q_start", "r_start")
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def aligner():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    a = sw.Aligner(0)
+    yield a
+    a.close()
+
+
+def oracle_batch(b: synth.Batch, threads=None):
+    return oracle.align_batch(b.queries, b.q_offsets, b.refs, b.r_offsets, b.scoring, threads=threads)
+
+
+def assert_parity(got: dict, exp: dict, b: synth.Batch):
+    """got/exp: five int32 arrays, one entry per pair of b."""
+    for f in FIELDS:
+        assert len(got[f]) == len(exp[f]) == b.n_pairs
+        bad = np.nonzero(got[f] != exp[f])[0]
+        if bad.size:
+            p = int(bad[0])
+            q, r = b.pair(p)
+            raise AssertionError(
+                f"field {f}: {bad.size} mismatches; first pair {p} (n={len(q)}, m={len(r)}): "
+                f"gpu={[int(got[k][p]) for k in FIELDS]} oracle={[int(exp[k][p]) for k in FIELDS]}\n"
+                f"q={q[:80]!r}\nr={r[:80]!r}")
+
+
+def run_and_compare(aligner, b: synth.Batch):
+    got = aligner.align(b)
+    exp = oracle_batch(b)
+    assert_parity(got, exp, b)
+    return got
+
+
+# ----------------------------------------------------------------- goldens
+
+def test_golden_examples(aligner):
+    rows = []
+    for l in open(os.path.join(GOLDEN, "worked_examples.tsv")):
+        if l.startswith("#") or not l.strip():
+            continue
+        p = l.rstrip("\n").split("\t")
+        rows.append(p)
+    for alpha in ("dna", "protein"):
+        sel = [p for p in rows if p[2] == alpha]
+        groups = {}
+        for p in sel:
+            groups.setdefault(tuple(p[3:7]), []).append(p)
+        for (ma, mm, o, e), ps in groups.items():
+            sc = {"alphabet": alpha, "match": int(ma), "mismatch": int(mm), "gap_open": int(o), "gap_extend": int(e)}
+            b = synth.from_pairs([(p[0], p[1]) for p in ps], sc)
+            got = aligner.align(b)
+            for k, p in enumerate(ps):
+                assert tuple(int(got[f][k]) for f in FIELDS) == tuple(int(x) for x in p[7:12]), p
+
+
+# ------------------------------------------------------- the five configs
+
+def test_c1_full_parity(aligner):
+    run_and_compare(aligner, synth.generate("c1"))
+
+
+def test_c2_prefix_parity(aligner):
+    run_and_compare(aligner, synth.generate("c2", 0, 4000))
+
+
+def test_c3_protein_prefix_parity(aligner):
+    run_and_compare(aligner, synth.generate("c3", 0, 1500))
+
+
+def test_c5_mixed_sample_parity(aligner):
+    """Length-skewed batch: multi-stripe queries up to 4 kb, references up to 16 kb."""
+    cfg = synth.CONFIGS["c5"]
+    n, m = synth.batch_lengths(cfg, 0, 4096)
+    longs = np.nonzero(n > 150)[0]
+    # a few long pairs of various sizes plus short ones, bounded oracle cost
+    cost = n[longs] * m[longs]
+    pick = list(longs[np.argsort(cost)][::max(1, len(longs) // 24)][:24]) + list(np.nonzero(n == 150)[0][:200])
+    full = synth.generate("c5", 0, 4096)
+    b = full.subset(sorted(int(p) for p in pick))
+    run_and_compare(aligner, b)
+
+
+def test_c2_full_size_sampled(aligner):
+    """C2 at its full BASELINE size in one call; 400 sampled pairs checked against the oracle."""
+    b = synth.generate("c2")
+    got = aligner.align(b)
+    rng = np.random.default_rng(2)
+    idx = np.sort(rng.choice(b.n_pairs, size=400, replace=False))
+    sub = b.subset(idx)
+    exp = oracle_batch(sub)
+    assert_parity({f: got[f][idx] for f in FIELDS}, exp, sub)
+    assert np.all(got["score"] > 0)
+
+
+# ------------------------------------------------------------ adversarial
+
+def test_tie_heavy_low_entropy(aligner):
+    pairs = []
+    rng = np.random.default_rng(11)
+    for L in (1, 2, 9, 10, 11, 31, 32, 33, 150, 159, 160, 161, 250, 319, 320, 321, 480):
+        pairs.append(("A" * L, "A" * (L + 7)))
+        pairs.append(("AC" * (L // 2 + 1), "CA" * (L // 2 + 3)))
+        pairs.append(("ACGT" * (L // 4 + 1), "ACGTACGT" * (L // 8 + 2)))
+        pairs.append(("".join(rng.choice(list("AC"), L)), "".join(rng.choice(list("AC"), L + 17))))
+    b = synth.from_pairs(pairs, synth.DNA_SCORING)
+    run_and_compare(aligner, b)
+    b = synth.from_pairs(pairs, {"alphabet": "dna", "match": 1, "mismatch": -1, "gap_open": -1, "gap_extend": -1})
+    run_and_compare(aligner, b)
+
+
+def test_random_small_many_scorings(aligner):
+    for k, (ma, mm, o, e) in enumerate([(3, -3, -6, -1), (2, -2, -1, -1), (1, -1, -2, -1), (2, -1, -3, -1),
+                                        (1, -1, -1, -1), (5, -4, -10, -2), (1, -3, -5, -2)]):
+        sc = {"alphabet": "dna", "match": ma, "mismatch": mm, "gap_open": o, "gap_extend": e}
+        b = synth.random_pairs(100 + k, 600, (0, 70), (0, 90), b"ACG" if k % 2 else b"ACGT", sc)
+        run_and_compare(aligner, b)
+
+
+def test_edge_cases_and_sentinels(aligner):
+    pairs = [("", ""), ("", "ACGT"), ("ACGT", ""), ("A", "A"), ("A", "C"), ("AAAA", "CCCC"),
+             ("ACNT", "ACGT"), ("ACGT", "ACGU"), ("acgt", "ACGT"), ("ACGT", "acgtacgt"), ("G" * 5000, "G" * 300)]
+    b = synth.from_pairs(pairs, synth.DNA_SCORING)
+    got = run_and_compare(aligner, b)
+    assert tuple(got["score"][:3]) == (0, 0, 0)
+    assert got["score"][6] == -1 and got["score"][7] == -1
+    st, nbad = aligner.batch_status()
+    assert st == sw.SW_ERR_BAD_PAIRS and nbad == 2
+
+
+def test_stripe_and_lane_boundaries(aligner):
+    """Queries around multiples of the 10-row lane block and the 160-row stripe."""
+    rng = np.random.default_rng(12)
+    pairs = []
+    for n in (1, 9, 10, 11, 159, 160, 161, 319, 320, 321, 479, 481, 1000):
+        for m in (1, 15, 16, 17, 200, 700):
+            q = "".join(rng.choice(list("ACGT"), n))
+            if m >= 10 and n >= 10:
+                s = rng.integers(0, n - 5)
+                r = "".join(rng.choice(list("ACGT"), m // 2)) + q[s:s + m // 2]
+                r = r[:m]
+            else:
+                r = "".join(rng.choice(list("ACGT"), m))
+            pairs.append((q, r))
+    run_and_compare(aligner, synth.from_pairs(pairs, synth.DNA_SCORING))
+
+
+def test_int32_routing_per_pair(aligner):
+    """s16-eligible scoring, but pairs whose max score exceeds the int16 bound go to the s32 kernel."""
+    sc = {"alphabet": "dna", "match": 30, "mismatch": -20, "gap_open": -40, "gap_extend": -5}
+    rng = np.random.default_rng(13)
+    pairs = []
+    for L in (1100, 1200):
+        q = "".join(rng.choice(list("ACGT"), L))
+        pairs.append((q, q[:L - 3] + "TTT"))            # near-identity: S ~ 30 L > 32000
+    for _ in range(40):
+        pairs.append(("".join(rng.choice(list("ACGT"), 60)), "".join(rng.choice(list("ACGT"), 90))))
+    got = run_and_compare(aligner, synth.from_pairs(pairs, sc))
+    assert got["score"][0] > 32767
+
+
+def test_int32_routing_whole_scoring(aligner):
+    """Scorings whose (s - gap_open) does not fit the int8 profile run entirely on the s32 kernel."""
+    sc = {"alphabet": "dna", "match": 100, "mismatch": -90, "gap_open": -150, "gap_extend": -7}
+    run_and_compare(aligner, synth.random_pairs(21, 300, (1, 400), (1, 500), b"ACGT", sc))
+    psc = {"alphabet": "protein", "gap_open": -200, "gap_extend": -3}
+    b = synth.generate("c3", 0, 200)
+    b.scoring = psc
+    run_and_compare(aligner, b)
+
+
+def test_protein_small_and_case(aligner):
+    pairs = [("HEAGAWGHEE", "PAWHEAE"), ("heagawghee", "pawheae"), ("MKTAYIAKQR*", "MKTAYIAKQR*"),
+             ("BZX*", "BZX*"), ("ACDJ", "ACD"), ("", "ACD")]
+    b = synth.from_pairs(pairs, synth.PROTEIN_SCORING)
+    got = run_and_compare(aligner, b)
+    assert got["score"][4] == -1
+
+
+# -------------------------------------------------------- batch invariance
+
+def test_permutation_and_shard_invariance(aligner):
+    """P11: results are a pure function of the pair (order, composition, sharding)."""
+    b = synth.generate("c1", 0, 600)
+    ref = aligner.align(b)
+    perm = np.random.default_rng(5).permutation(b.n_pairs)
+    got = aligner.align(b.subset(perm))
+    for f in FIELDS:
+        np.testing.assert_array_equal(got[f], ref[f][perm])
+    cuts = sw.sw_plan_shards(b.q_offsets, b.r_offsets, 3)
+    for k in range(3):
+        part = aligner.align(b.subset(range(cuts[k], cuts[k + 1])))
+        for f in FIELDS:
+            np.testing.assert_array_equal(part[f], ref[f][cuts[k]:cuts[k + 1]])
+    again = aligner.align(b)
+    for f in FIELDS:
+        np.testing.assert_array_equal(again[f], ref[f])
+
+
+def test_host_entry_point_matches_device_entry_point(aligner):
+    import torch
+    b = synth.generate("c1", 0, 300)
+    ref = aligner.align(b)
+    out = {f: np.zeros(b.n_pairs, np.int32) for f in FIELDS}
+    qa, ra = np.ascontiguousarray(b.queries), np.ascontiguousarray(b.refs)
+    qo, ro = np.ascontiguousarray(b.q_offsets), np.ascontiguousarray(b.r_offsets)
+    st = sw.sw_align_batch_host(aligner.handle, qa.ctypes.data, qo.ctypes.data, ra.ctypes.data, ro.ctypes.data,
+                                b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS},
+                                torch.cuda.current_stream().cuda_stream)
+    assert st == sw.SW_OK
+    for f in FIELDS:
+        np.testing.assert_array_equal(out[f], ref[f])
+
+
+def test_offsets_need_not_start_at_zero(aligner):
+    import torch
+    b = synth.generate("c1", 0, 50)
+    ref = aligner.align(b)
+    q, qo, r, ro = aligner.to_device(b)
+    pad = torch.zeros(100, dtype=torch.uint8, device="cuda:0")
+    q2 = torch.cat([pad, q]); r2 = torch.cat([pad, r])
+    out, st = aligner.align_tensors(q2, qo + 100, r2, ro + 100, b.scoring)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    for i, f in enumerate(FIELDS):
+        np.testing.assert_array_equal(o[i, :50], ref[f])
+
+
+# --------------------------------------------------------------- ABI errors
+
+def test_abi_errors(aligner):
+    import torch
+    b = synth.generate("c1", 0, 10)
+    q, qo, r, ro = aligner.to_device(b)
+    bad_sc = dict(b.scoring, gap_open=1)
+    out, st = aligner.align_tensors(q, qo, r, ro, bad_sc, check=False)
+    assert st == sw.SW_ERR_INVALID_SCORING
+    out, st = aligner.align_tensors(q, qo, r, ro, dict(b.scoring, gap_extend=-7), check=False)
+    assert st == sw.SW_ERR_INVALID_SCORING
+    out, st = aligner.align_tensors(q, qo, r, ro, dict(b.scoring, match=-1), check=False)
+    assert st == sw.SW_ERR_INVALID_SCORING
+    # decreasing offsets -> invalid argument, every field -1
+    qo_bad = qo.clone(); qo_bad[3] = qo_bad[5] + 1
+    out, st = aligner.align_tensors(q, qo_bad, r, ro, b.scoring, check=False)
+    torch.cuda.synchronize()
+    assert st == sw.SW_ERR_INVALID_ARGUMENT
+    assert (out[:, :10] == -1).all()
+    # zero pairs: no-op
+    out, st = aligner.align_tensors(q, qo[:1], r, ro[:1], b.scoring, check=False)
+    assert st == sw.SW_OK
+    # the handle still works afterwards
+    got = aligner.align(b)
+    np.testing.assert_array_equal(got["score"], oracle_batch(b)["score"])
+
+
+def test_dpx_peak_probe_runs():
+    import torch
+    cups = sw.sw_dpx_peak(0, 50.0, torch.cuda.current_stream().cuda_stream)
+    assert 1e12 < cups < 5e13

@@ -1,0 +1,129 @@
+// tools/dpx_probe.cu -- issue-rate probe for the integer/DPX instructions the
+// Smith-Waterman inner loop uses (VIADDMNMX.S16x2, VIMNMX(3).S16x2, VIADD,
+// PRMT, IMAD, LOP3, SHFL).  Standalone: nvcc -gencode arch=compute_100a,code=sm_100a.
+// Prints, per probe, warp-instructions issued per SM clock (clock64 based, so
+// independent of the SM frequency) and the wall-clock rate.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CHAINS 8
+#define ITERS 4096
+
+struct Out { unsigned long long cycles; unsigned v; };
+
+__device__ __forceinline__ unsigned prmt(unsigned a, unsigned b, unsigned s) {
+    unsigned d; asm volatile("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s)); return d;
+}
+
+// variant 0: 5.5-instruction Gotoh cell-pair mix (the roofline mix)
+// variant 1: VIADDMNMX.S16x2 only
+// variant 2: VIMNMX3.S16x2 only
+// variant 3: PRMT only
+// variant 4: IMAD only
+// variant 5: mix + 1 PRMT per cell pair (6.5)
+// variant 6: mix with the H+o add done by IMAD (FMA pipe)
+// variant 7: VIADDMNMX + IMAD interleaved 1:1
+// variant 8: LOP3 only
+// variant 9: SHFL only
+template <int V>
+__global__ void probe(Out* out, unsigned seed, unsigned o2, unsigned e2) {
+    unsigned h[CHAINS], e[CHAINS], f[CHAINS], x[CHAINS];
+    unsigned best = 0;
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) {
+        h[c] = seed * (c + 1) + threadIdx.x; e[c] = h[c] ^ 0x5555; f[c] = h[c] + 77; x[c] = h[c] * 3;
+    }
+    unsigned s = seed ^ 0x00030003u;
+    __syncthreads();
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) {
+            if (V == 0 || V == 5 || V == 6) {
+                unsigned ho;
+                if (V == 6) ho = h[c] * seed + o2; else ho = __vadd2(h[c], o2);
+                e[c] = __viaddmax_s16x2(e[c], e2, ho);
+                f[c] = __viaddmax_s16x2(f[c], e2, ho);
+                unsigned t = __vimax_s16x2_relu(e[c], f[c]);
+                unsigned sc = s;
+                if (V == 5) sc = prmt(x[c], s, 0x3210 + (c & 3));
+                h[c] = __viaddmax_s16x2_relu(x[c], sc, t);
+                x[c] = h[c];
+                if (c & 1) best = __vimax3_s16x2_relu(best, h[c], h[c - 1]);
+            } else if (V == 1) {
+                h[c] = __viaddmax_s16x2(h[c], e2, e[c]);
+            } else if (V == 2) {
+                h[c] = __vimax3_s16x2_relu(h[c], e[c], f[c]);
+                e[c] ^= h[c];
+            } else if (V == 3) {
+                h[c] = prmt(h[c], e[c], s + c);
+            } else if (V == 4) {
+                h[c] = h[c] * seed + e[c];
+            } else if (V == 7) {
+                h[c] = __viaddmax_s16x2(h[c], e2, e[c]);
+                x[c] = x[c] * seed + f[c];
+            } else if (V == 8) {
+                h[c] = (h[c] & e[c]) ^ f[c];
+                f[c] = (f[c] | h[c]) ^ e[c];
+            } else if (V == 9) {
+                h[c] = __shfl_up_sync(0xffffffffu, h[c], 1, 16);
+            }
+        }
+    }
+    unsigned long long t1 = clock64();
+    unsigned acc = best;
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) acc ^= h[c] ^ e[c] ^ f[c] ^ x[c];
+    if (threadIdx.x % 32 == 0) {
+        Out* o = out + (blockIdx.x * blockDim.x + threadIdx.x) / 32;
+        o->cycles = t1 - t0;
+        o->v = acc;
+    }
+}
+
+// instructions per chain-iteration (per thread) that the probe is meant to measure
+static const double INSTR_PER_CHAIN[10] = {5.5, 1, 1, 1, 1, 6.5, 5.5, 2, 2, 1};
+static const char* NAMES[10] = {"mix5.5(s16x2 gotoh)", "VIADDMNMX.S16x2", "VIMNMX3.S16x2(+LOP)", "PRMT", "IMAD",
+                                "mix+PRMT(6.5)", "mix,IMAD for H+o", "VIADDMNMX+IMAD", "LOP3 x2", "SHFL"};
+
+template <int V>
+void run(int sms, int blocks_per_sm, int threads) {
+    int grid = sms * blocks_per_sm;
+    int warps = grid * threads / 32;
+    Out* d; cudaMalloc(&d, sizeof(Out) * warps);
+    probe<V><<<grid, threads>>>(d, 3, 0xFFFAFFFAu, 0xFFFFFFFFu);  // warm
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    probe<V><<<grid, threads>>>(d, 3, 0xFFFAFFFAu, 0xFFFFFFFFu);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    Out* h = new Out[warps];
+    cudaMemcpy(h, d, sizeof(Out) * warps, cudaMemcpyDeviceToHost);
+    double cyc = 0; for (int w = 0; w < warps; ++w) cyc += h[w].cycles; cyc /= warps;
+    double winstr_per_warp = INSTR_PER_CHAIN[V] * CHAINS * ITERS;
+    int warps_per_sm = blocks_per_sm * threads / 32;
+    double ipc = winstr_per_warp * warps_per_sm / cyc;   // warp-instr / SM clock
+    double wall_rate = winstr_per_warp * warps / (ms * 1e-3);  // warp-instr / s (whole GPU)
+    double mhz = (cyc / (ms * 1e-3)) / 1e6;
+    printf("%-22s warps/SM=%2d  warp-instr/clk/SM=%.3f  GPU warp-instr/s=%.3e  implied SM MHz=%.0f  ms=%.3f\n",
+           NAMES[V], warps_per_sm, ipc, wall_rate, mhz, ms);
+    if (V == 0 || V == 5 || V == 6) {
+        double cellpairs = (double)CHAINS * ITERS * 32.0 * warps;
+        printf("    -> cell updates/s (2 cells per s16x2 chain step) = %.3f TCUPS\n", 2 * cellpairs / (ms * 1e-3) / 1e12);
+    }
+    delete[] h; cudaFree(d);
+}
+
+int main() {
+    cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+    printf("device %s SMs=%d clockRate(kHz)=%d\n", p.name, p.multiProcessorCount, p.clockRate);
+    int sms = p.multiProcessorCount;
+    for (int bps : {2, 4, 8}) {
+        printf("--- blocks/SM=%d x 256 threads\n", bps);
+        run<0>(sms, bps, 256); run<1>(sms, bps, 256); run<2>(sms, bps, 256); run<3>(sms, bps, 256);
+        run<4>(sms, bps, 256); run<5>(sms, bps, 256); run<6>(sms, bps, 256); run<7>(sms, bps, 256);
+        run<8>(sms, bps, 256); run<9>(sms, bps, 256);
+    }
+    return 0;
+}
