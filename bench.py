@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""Benchmark: batched Smith-Waterman (affine gaps) GCUPS on B200, one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "ADEPT-shaped DNA batch: 100k pairs, 150 bp
+reads vs contigs up to 1,024 bp, 1 B200"): the seeded synthetic batch of
+paper_2208_12350_b200.synth config "c2" (3/-3/-6/-1).  At N GPUs (torchrun, one
+rank per GPU) the global batch is c2 followed by the first (N-1)*100k pairs of
+config "c4" (the same recipe, BASELINE configs[3]), cut into N contiguous
+cell-balanced shards by sw_plan_shards: per-GPU work is fixed -> weak scaling.
+
+A step = one sw_align_batch call (pack, binning, forward wavefront, reverse
+wavefront, finish) over the rank's shard, inputs resident in HBM; L2 (126 MB)
+is flushed between steps (a 512 MB write outside the timed events).  Time =
+sum of per-step CUDA-event times on the call's stream, max over ranks.
+`e2e` repeats the measurement through sw_align_batch_host: pinned host inputs
+-> H2D -> align -> D2H of the five result arrays, every step.
+
+--impl reference runs the CPU oracle (oracle/, plain full-matrix C, all host
+cores) on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GCUPS (DNA and protein batches) at 1/2/4/8 B200; % of DPX cell-update roofline"
+PAIRS_PER_GPU = 100_000
+FIELDS = ("score", "q_end", "r_end", "q_start", "r_start")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-extra", action="store_true", help="skip the protein / C1 side measurements")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ workload
+
+def global_lengths(n_gpus: int):
+    from paper_2208_12350_b200 import synth
+    n2, m2 = synth.batch_lengths(synth.CONFIGS["c2"])
+    if n_gpus == 1:
+        return n2, m2
+    n4, m4 = synth.batch_lengths(synth.CONFIGS["c4"], 0, (n_gpus - 1) * PAIRS_PER_GPU)
+    return np.concatenate([n2, n4]), np.concatenate([m2, m4])
+
+
+def shard_range(n_gpus: int, rank: int):
+    from paper_2208_12350_b200 import sw
+    n, m = global_lengths(n_gpus)
+    qo = np.zeros(n.size + 1, np.int64); qo[1:] = np.cumsum(n)
+    ro = np.zeros(m.size + 1, np.int64); ro[1:] = np.cumsum(m)
+    cuts = sw.sw_plan_shards(qo, ro, n_gpus)
+    return int(cuts[rank]), int(cuts[rank + 1]), n.size
+
+
+def make_shard(lo: int, hi: int):
+    """Pairs [lo, hi) of the global batch (c2 then c4)."""
+    from paper_2208_12350_b200 import synth
+    parts = []
+    c2n = synth.CONFIGS["c2"].n_pairs
+    if lo < c2n:
+        parts.append(synth.generate("c2", lo, min(hi, c2n)))
+    if hi > c2n:
+        parts.append(synth.generate("c4", max(lo, c2n) - c2n, hi - c2n))
+    if len(parts) == 1:
+        return parts[0]
+    a, b = parts
+    qo = np.concatenate([a.q_offsets, b.q_offsets[1:] + a.q_offsets[-1]])
+    ro = np.concatenate([a.r_offsets, b.r_offsets[1:] + a.r_offsets[-1]])
+    return synth.Batch(np.concatenate([a.queries, b.queries]), qo, np.concatenate([a.refs, b.refs]), ro,
+                       a.scoring, "c2+c4")
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            p = [x.strip() for x in l.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0])); smax.append(float(p[1])); power.append(float(p[2]))
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if p[4 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s, w in zip(sm, power) if w > 250] or sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": float(max(power))}
+
+
+# ------------------------------------------------------------------ oracle leg
+
+def oracle_sample(batch, budget_s: float = 15.0):
+    """Time the oracle as it stands on a bounded prefix of `batch` (about budget_s of work)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    k = min(batch.n_pairs, 256)
+    sub = batch.subset(range(k))
+    t = time.perf_counter()
+    oracle.align_batch(sub.queries, sub.q_offsets, sub.refs, sub.r_offsets, sub.scoring, threads=cores)
+    dt = time.perf_counter() - t
+    k2 = int(min(batch.n_pairs, max(k, k * budget_s / max(dt, 1e-3))))
+    sub = batch.subset(range(k2))
+    t = time.perf_counter()
+    out = oracle.align_batch(sub.queries, sub.q_offsets, sub.refs, sub.r_offsets, sub.scoring, threads=cores)
+    dt = time.perf_counter() - t
+    return sub, out, dt, cores
+
+
+# ------------------------------------------------------------------ main legs
+
+def run_reference(args, rank: int):
+    from paper_2208_12350_b200 import synth
+    if rank != 0:
+        return
+    b = synth.generate("c2", 0, 20_000)
+    import oracle
+    cores = os.cpu_count() or 1
+    # each step = a bounded prefix sample sized to ~6 s of oracle work
+    k = 256
+    sub = b.subset(range(k))
+    t = time.perf_counter()
+    oracle.align_batch(sub.queries, sub.q_offsets, sub.refs, sub.r_offsets, sub.scoring, threads=cores)
+    dt = time.perf_counter() - t
+    k = int(min(b.n_pairs, max(256, k * 6.0 / max(dt, 1e-3))))
+    sub = b.subset(range(k))
+    cells = sub.cells()
+    for _ in range(args.warmup):
+        oracle.align_batch(sub.queries, sub.q_offsets, sub.refs, sub.r_offsets, sub.scoring, threads=cores)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.align_batch(sub.queries, sub.q_offsets, sub.refs, sub.r_offsets, sub.scoring, threads=cores)
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = cells * args.steps / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GCUPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "c2_dna_100k_150x1024 (BASELINE configs[1]) -- bounded prefix sample per step",
+                   "pairs_per_step": sub.n_pairs, "cells_per_step": cells, "scoring": "3/-3/-6/-1"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+                         "sample": f"first {sub.n_pairs} pairs of c2 ({cells:.3e} forward cells), forward+reverse"},
+        "e2e": {"value": round(value, 4), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_device_steps(a, q, qo, r, ro, scoring, out, steps, warmup, flush_buf, torch):
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        a.align_tensors(q, qo, r, ro, scoring, out=out)
+    torch.cuda.synchronize()
+    times, stage = [], []
+    for _ in range(steps):
+        flush_buf.zero_()  # evict L2 between steps (outside the timed events)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        a.align_tensors(q, qo, r, ro, scoring, out=out)
+        e1.record(s)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        stage.append(a.stage_ms())
+    return times, stage
+
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+    from paper_2208_12350_b200 import sw, synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device(f"cuda:{local_rank}")
+    lo, hi, n_global = shard_range(world, rank)
+    batch = make_shard(lo, hi)
+    cells = batch.cells()
+    a = sw.Aligner(local_rank)
+    a.enable_stage_timing(True)
+    q, qo, r, ro = a.to_device(batch)
+    out = a.alloc_out(batch.n_pairs)
+    flush_buf = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    # roofline denominator: measured DPX Gotoh-mix rate on this GPU, same process
+    peak_cups = sw.sw_dpx_peak(local_rank, 300.0, torch.cuda.current_stream().cuda_stream)
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    times, stages = time_device_steps(a, q, qo, r, ro, batch.scoring, out, args.steps, args.warmup, flush_buf, torch)
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    own, lib = a.launch_count()
+    st, nbad = a.batch_status()
+    fwd_cells, swept = a.cell_counts()
+    total_ms = float(sum(times))
+    stage_med = {k: float(np.median([x[k] for x in stages])) for k in stages[0]}
+
+    # ---- e2e through the host entry point (pinned host buffers) ----
+    qh = torch.from_numpy(np.ascontiguousarray(batch.queries)).pin_memory()
+    rh = torch.from_numpy(np.ascontiguousarray(batch.refs)).pin_memory()
+    qoh = torch.from_numpy(np.ascontiguousarray(batch.q_offsets)).pin_memory()
+    roh = torch.from_numpy(np.ascontiguousarray(batch.r_offsets)).pin_memory()
+    outh = torch.empty((5, batch.n_pairs), dtype=torch.int32).pin_memory()
+    ptrs = {f: outh[i].data_ptr() for i, f in enumerate(FIELDS)}
+    s = torch.cuda.current_stream()
+
+    def host_call():
+        rc = sw.sw_align_batch_host(a.handle, qh.data_ptr(), qoh.data_ptr(), rh.data_ptr(), roh.data_ptr(),
+                                    batch.n_pairs, batch.scoring, ptrs, s.cuda_stream)
+        if rc != sw.SW_OK:
+            raise sw.SWError(rc, sw.sw_last_error_message(a.handle))
+
+    for _ in range(max(1, args.warmup)):
+        host_call()
+    e2e_times = []
+    for _ in range(args.steps):
+        flush_buf.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        host_call()
+        e1.record(s)
+        e1.synchronize()
+        e2e_times.append(e0.elapsed_time(e1))
+    e2e_total = float(sum(e2e_times))
+    # results of the host path must equal the device path
+    same = bool(torch.equal(outh, out[:, :batch.n_pairs].cpu()))
+
+    # ---- aggregate over ranks: max time ----
+    vals = torch.tensor([total_ms, e2e_total, stage_med["fwd"]], dtype=torch.float64, device=dev)
+    cells_t = torch.tensor([cells, fwd_cells], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cells_t, op=dist.ReduceOp.SUM)
+    total_ms, e2e_total, fwd_ms_max = [float(x) for x in vals.tolist()]
+    all_cells = float(cells_t[0].item())
+
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        for key in ("c3", "c1"):
+            bx = synth.generate(key) if key == "c1" else synth.generate(key)
+            qx, qox, rx, rox = a.to_device(bx)
+            ox = a.alloc_out(bx.n_pairs)
+            tx, sx = time_device_steps(a, qx, qox, rx, rox, bx.scoring, ox, 3, 2, flush_buf, torch)
+            med = float(np.median(tx))
+            extra[key] = {"workload": synth.CONFIGS[key].name, "gcups": round(bx.cells() / med / 1e6, 1),
+                          "ms": round(med, 3), "fwd_kernel_gcups": round(bx.cells() / float(np.median([x["fwd"] for x in sx])) / 1e6, 1),
+                          "stage_ms": {k: round(float(np.median([x[k] for x in sx])), 4) for k in sx[0]}}
+
+    cpu = None
+    parity = None
+    if rank == 0 and not args.no_cpu_baseline:
+        sub, o, dt, cores = oracle_sample(batch)
+        cpu = {"value": round(sub.cells() / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+               "sample": f"first {sub.n_pairs} pairs of the rank-0 shard ({sub.cells():.3e} forward cells), "
+                         f"forward+reverse, {dt:.1f} s"}
+        gpu = out[:, :sub.n_pairs].cpu().numpy()
+        mism = sum(int(np.sum(gpu[i] != o[f])) for i, f in enumerate(FIELDS))
+        parity = f"{sub.n_pairs} pairs x 5 fields vs oracle: {mism} mismatches"
+
+    if rank != 0:
+        a.close()
+        return
+    value = all_cells * args.steps / (total_ms * 1e-3) / 1e9
+    fwd_gcups = cells / (stage_med["fwd"] * 1e-3) / 1e9  # rank-0 dominant kernel, live events
+    peak_gcups = peak_cups / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_fwd_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    h2d = int(batch.queries.nbytes + batch.refs.nbytes + batch.q_offsets.nbytes + batch.r_offsets.nbytes)
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "GCUPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(total_ms / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int16",
+        "data": "synthetic",
+        "config": {"workload": "c2_dna_100k_150x1024 (BASELINE configs[1])" if world == 1 else
+                   f"c2 + c4[:{(world - 1) * PAIRS_PER_GPU}] = {n_global} pairs, cell-balanced shards",
+                   "pairs": n_global, "pairs_per_gpu": batch.n_pairs, "cells_per_gpu": cells,
+                   "scoring": "DNA 3/-3/-6/-1", "step": "sw_align_batch: pack+bin+fwd+rev+finish",
+                   "l2": "flushed between steps (512 MB write outside timed events)",
+                   "parallelism": f"dp{world}"},
+        "roofline": {"bound": "alu", "achieved": round(fwd_gcups, 1), "peak": round(peak_gcups, 1), "unit": "GCUPS",
+                     "frac": round(fwd_gcups / peak_gcups, 4), "traffic": traffic,
+                     "kernel": "wavefront_kernel<TS16,16,10,fwd>",
+                     "peak_source": "sw_dpx_peak: measured s16x2 Gotoh 5.5-instr cell-pair mix, this GPU, this run",
+                     "peak_derived_gcups": round(148 * 2 * 32 * 1.965e9 * 2 / 5.5 / 1e9, 1)},
+        "e2e": {"value": round(all_cells * args.steps / (e2e_total * 1e-3) / 1e9, 1), "unit": "GCUPS",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 5 * 4 * batch.n_pairs,
+                "matches_device_path": same},
+        "gpu_launches": int(own * args.steps),
+        "library_sort_calls": int(lib * args.steps),
+        "clocks": clk,
+        "stage_ms": {k: round(v, 4) for k, v in stage_med.items()},
+        "swept_over_real_cells": round(swept / max(fwd_cells, 1), 4),
+        "status": {"batch_status": sw.status_string(st), "bad_pairs": nbad},
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+        line["parity_sample"] = parity
+    if extra:
+        line["extra"] = extra
+    a.close()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -67,6 +67,7 @@ struct sw_context {
     DevBuf<int64_t> st_qo, st_ro;
     DevBuf<int32_t> st_out;
 
+    int codes_alphabet = -1;  // alphabet the code buffers were last cleared for
     bool timing = false;
     cudaEvent_t ev[8] = {};
     bool ev_valid = false;
@@ -227,7 +228,18 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     ENS(nlen, N); ENS(mlen, N); ENS(nlen_rev, N); ENS(mlen_rev, N); ENS(target, N); ENS(iota, N);
     ENS(order, N); ENS(order_rev, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
     ENS(keys_fwd, N); ENS(keys_rev, N);
-    ENS(qcode, tq + 16); ENS(qrev, tq + 16); ENS(rcode, rbytes); ENS(rrev, rbytes);
+    ENS(qcode, tq + 16); ENS(qrev, tq + 16);
+    {
+        // Every byte of the reference code buffers must be a valid code of the batch's
+        // alphabet: finished halves of a work item keep reading past their reference.
+        uint8_t* old_r = h->rcode.p; uint8_t* old_rr = h->rrev.p;
+        ENS(rcode, rbytes); ENS(rrev, rbytes);
+        if (h->rcode.p != old_r || h->rrev.p != old_rr || h->codes_alphabet != sc.alphabet) {
+            SW_CUDA(h, cudaMemsetAsync(h->rcode.p, 0, h->rcode.cap, s));
+            SW_CUDA(h, cudaMemsetAsync(h->rrev.p, 0, h->rrev.cap, s));
+            h->codes_alphabet = sc.alphabet;
+        }
+    }
     {
         size_t tb = 0;
         cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p, h->key_sorted.p, h->iota.p, h->order.p,

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
             for (int64_t j = lane; j < m; j += 32) {
                 uint8_t c = P.alphabet == SW_ALPHABET_DNA ? dna_code(P.refs[ra + j]) : protein_code(P.refs[ra + j]);
                 bad |= (c == CODE_BAD);
-                P.rcode[rp + j] = c;
+                P.rcode[rp + j] = (c == CODE_BAD) ? pad_code : c;  // the wavefront indexes the profile by code
             }
             // pads around the reference, in both the forward and the reverse buffer
             for (int k = lane; k < PADL + PADR; k += 32) {

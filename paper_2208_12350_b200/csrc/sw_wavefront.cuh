@@ -80,13 +80,206 @@ struct LaneState {
     uint32_t E[K];    // E of the lane's rows at the previous column
     uint32_t SV[K];   // HO of the column where the lane's best last improved
 };
+// Opaque copy of a value (keeps ptxas from turning `x * flag + b` back into a
+// SEL on the ALU pipe: the multiply-add then issues on the FMA pipe).
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    uint32_t y;
+    asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
+
+// Reference code byte into a full 32-bit register (read-only path).  An asm
+// load keeps ptxas from packing the prefetched codes into shared registers
+// with PRMT (ALU-pipe work on every column).
+__device__ __forceinline__ uint32_t ld_code(const uint8_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+
+// One stripe of one work item: the column sweep of the anti-diagonal
+// wavefront for this lane's K rows of both halves.  MULTI adds the stripe
+// hand-off (boundary row in from scratch, bottom row out to scratch).
+template <class T, int W, int K, bool REV, bool MULTI>
+__device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const int seg,
+                                      const int L, const int s_m, const int (&h_pid)[T::NH], const int (&h_m)[T::NH],
+                                      const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH], const int mmax,
+                                      const int row0, const uint32_t o2, const uint32_t e2, const int o,
+                                      const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch) {
+    using G = Geometry<W, K, T>;
+    constexpr int NH = T::NH;
+    constexpr int SLOTS = G::SLOTS;
+    constexpr int U = 4;                 // column unroll
+    constexpr int CS = W * G::PB;        // profile bytes per code
+    const int nc = P.sc.nc;
+
+    uint32_t HO[K], E[K], SV[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) { HO[r] = o2; E[r] = o2; SV[r] = 0; }
+    uint32_t best = 0, bestcol = 0;
+    uint32_t hoLast = o2, fLast = o2, prevUpHO = o2;
+    int ev[NH];
+    int next_ev = 0x7fffffff;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        ev[h] = (!REV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
+        next_ev = min(next_ev, ev[h]);
+    }
+    uint32_t prof_h[NH];  // shared-window address of this lane's profile entries, code 0
+    const uint8_t* rp[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        prof_h[h] = (uint32_t)__cvta_generic_to_shared(prof + (size_t)(seg * NH + h) * nc * CS + (size_t)L * G::PB);
+        rp[h] = P.rcode + h_rpos[h] - L;  // this lane's column 0 (pad codes before it)
+    }
+    const uint32_t cs = opaque(CS);  // code stride as a runtime value: the address is one IMAD
+    // lane 0 takes the row above from the stripe boundary: up = shfl * notL0 + b (IMAD)
+    const uint32_t notL0 = opaque(L != 0 ? 1u : 0u);
+    const uint32_t b0 = (L == 0) ? o2 : 0u;
+
+    // rotating prefetch of the next U columns' codes (and boundary rows)
+    uint32_t cd[U][NH];
+    uint2 bnd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) cd[u][h] = ld_code(rp[h] + u);
+        if (MULTI) bnd[u] = (from_scratch && L == 0) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
+    }
+
+    int T_end = mmax + W - 1;
+    if (REV) {
+        int te = 0;
+#pragma unroll
+        for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_m, sl) + W - 1, stop[sl]));
+        T_end = te;
+    }
+    for (int t0 = 0; t0 < T_end; t0 += U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int t = t0 + u;
+            // query-profile words of this lane's column (all K rows, both halves)
+            uint32_t pw[NH][G::PWORDS];
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const uint32_t src = prof_h[h] + cd[u][h] * cs;
+#pragma unroll
+                for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
+                    const uint4 v = lds128(src + 16 * q4);
+                    pw[h][q4 * 4 + 0] = v.x; pw[h][q4 * 4 + 1] = v.y;
+                    pw[h][q4 * 4 + 2] = v.z; pw[h][q4 * 4 + 3] = v.w;
+                }
+                cd[u][h] = ld_code(rp[h] + t + U);
+            }
+            uint32_t bHO = b0, bF = b0;
+            if (MULTI) {
+                bHO = bnd[u].x; bF = bnd[u].y;
+                bnd[u] = (from_scratch && L == 0) ? __ldcg(scr_in + t + U) : make_uint2(b0, b0);
+            }
+            // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
+            const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
+            const uint32_t upF = __shfl_up_sync(FULL, fLast, 1, W) * notL0 + bF;
+            uint32_t hd = prevUpHO;
+            prevUpHO = upHO;
+            uint32_t F = upF, hu = upHO;
+            uint32_t H[K];
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                uint32_t sc;
+                if (NH == 2) {
+                    constexpr uint32_t SEL[4] = {0xC480u, 0xD591u, 0xE6A2u, 0xF7B3u};
+                    sc = prmt(pw[0][r >> 2], pw[NH - 1][r >> 2], SEL[r & 3]);
+                } else {
+                    sc = pw[0][r];
+                }
+                E[r] = T::addmax(E[r], e2, HO[r]);          // E[i][j] = max(E[i][j-1] + e, H[i][j-1] + o)
+                F = T::addmax(F, e2, hu);                   // F[i][j] = max(F[i-1][j] + e, H[i-1][j] + o)
+                const uint32_t tt = T::max_relu(E[r], F);   // max(E, F, 0)
+                const uint32_t h = T::addmax(hd, sc, tt);   // max(H[i-1][j-1] + s, E, F, 0)
+                hd = HO[r];
+                HO[r] = T::add(h, o2);
+                hu = HO[r];
+                H[r] = h;
+            }
+            hoLast = HO[K - 1];
+            fLast = F;
+            // running max over the lane's rows; strict improvement -> remember column + HO values
+            uint32_t nb = best;
+#pragma unroll
+            for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
+            if (K & 1) nb = T::max2(nb, H[K - 1]);
+            if (nb != best) {
+                const uint32_t mask = T::changed_mask(nb, best);
+#pragma unroll
+                for (int r = 0; r < K; ++r) SV[r] = (SV[r] & ~mask) | (HO[r] & mask);
+                bestcol = (bestcol & ~mask) | (T::splat(t - L) & mask);
+                best = nb;
+                if (REV) {
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        if (h_pid[h] >= 0 && T::get(mask, h) != 0 && T::get(best, h) == h_tgt[h]) {
+                            int rr = 0;
+#pragma unroll
+                            for (int r = K - 1; r >= 0; --r) if (T::get(SV[r], h) == h_tgt[h] + o) rr = r;
+                            const int j = t - L;
+                            const int i = row0 + L * K + rr;
+                            const unsigned long long key = ((unsigned long long)(uint32_t)h_tgt[h] << 32) |
+                                ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
+                            atomicMax(P.keys + h_pid[h], key);
+                            atomicMin((int*)stop + seg * NH + h, j + W);
+                        }
+                    }
+                }
+            }
+            if (!REV && t == next_ev) {
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    if (ev[h] == t) {
+                        const int b = T::get(best, h);
+                        if (b > 0) {
+                            int rr = 0;
+#pragma unroll
+                            for (int r = K - 1; r >= 0; --r) if (T::get(SV[r], h) == b + o) rr = r;
+                            const int j = (NH == 2) ? (int)((bestcol >> (16 * h)) & 0xffff) : (int)bestcol;
+                            const int i = row0 + L * K + rr;
+                            const unsigned long long key = ((unsigned long long)(uint32_t)b << 32) |
+                                ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
+                            atomicMax(P.keys + h_pid[h], key);
+                        }
+                        best = T::set(best, h, T::FROZEN);
+                        ev[h] = 0x7fffffff;
+                    }
+                }
+                next_ev = ev[0];
+                if (NH == 2) next_ev = min(next_ev, ev[NH - 1]);
+            }
+            if (MULTI && to_scratch && L == W - 1) {
+                const int c = t - (W - 1);
+                if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
+            }
+        }
+        if (REV) {
+            __syncwarp();
+            int te = 0;
+#pragma unroll
+            for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_m, sl) + W - 1, stop[sl]));
+            T_end = te;
+        }
+    }
+}
+
 
 template <class T, int W, int K, bool REV>
 __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
-    constexpr int U = 4;  // column unroll
     extern __shared__ __align__(16) uint8_t smem[];
 
     const int lane = threadIdx.x & 31;
@@ -199,173 +392,17 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
             }
             __syncwarp();
 
-            // ---- per-stripe lane state ----
-            LaneState<T, K> st;
-#pragma unroll
-            for (int r = 0; r < K; ++r) { st.HO[r] = o2; st.E[r] = o2; st.SV[r] = 0; }
-            uint32_t best = 0, bestcol = 0;
-            uint32_t hoLast = o2, fLast = o2, prevUpHO = o2;
-            int ev[NH];
-            int next_ev = 0x7fffffff;
-#pragma unroll
-            for (int h = 0; h < NH; ++h) {
-                ev[h] = (!REV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
-                next_ev = min(next_ev, ev[h]);
-            }
-            const bool from_scratch = s > 0;
-            const bool to_scratch = s + 1 < ns;
-            const uint2* scr_in = reinterpret_cast<const uint2*>(P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes);
-            uint2* scr_out = reinterpret_cast<uint2*>(P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
-            const uint8_t* prof_h[NH];
-#pragma unroll
-            for (int h = 0; h < NH; ++h) prof_h[h] = prof + (size_t)(seg * NH + h) * nc * W * G::PB + (size_t)L * G::PB;
-            const size_t code_stride = (size_t)W * G::PB;
-
-            // prefetch of reference codes and boundary rows, one U-block ahead.  Codes are
-            // clamped to the profile: a finished (frozen) half keeps reading past its
-            // reference into bytes that may be stale or CODE_BAD.
-            uint8_t cd[U][NH];
-            uint2 bnd[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-#pragma unroll
-                for (int h = 0; h < NH; ++h) cd[u][h] = (uint8_t)min((int)P.rcode[h_rpos[h] + (u - L)], nc - 1);
-                bnd[u] = (from_scratch && L == 0) ? __ldcg(scr_in + u) : make_uint2(o2, o2);
-            }
-
-            int T_end = T_steps;
-            if (REV) {
-                int te = 0;
-#pragma unroll
-                for (int sl = 0; sl < SLOTS; ++sl) {
-                    const int m_sl = __shfl_sync(FULL, s_m, sl);
-                    te = max(te, min(m_sl + W - 1, stop[sl]));
-                }
-                T_end = te;
-            }
-            for (int t0 = 0; t0 < T_end; t0 += U) {
-                uint8_t cdn[U][NH];
-                uint2 bndn[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-#pragma unroll
-                    for (int h = 0; h < NH; ++h) cdn[u][h] = (uint8_t)min((int)P.rcode[h_rpos[h] + (t0 + U + u - L)], nc - 1);
-                    bndn[u] = (from_scratch && L == 0) ? __ldcg(scr_in + t0 + U + u) : make_uint2(o2, o2);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int t = t0 + u;
-                    // profile words of this lane's column, both halves
-                    uint32_t pw[NH][G::PWORDS];
-#pragma unroll
-                    for (int h = 0; h < NH; ++h) {
-                        const uint4* src = reinterpret_cast<const uint4*>(prof_h[h] + cd[u][h] * code_stride);
-#pragma unroll
-                        for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
-                            uint4 v = src[q4];
-                            pw[h][q4 * 4 + 0] = v.x; pw[h][q4 * 4 + 1] = v.y;
-                            pw[h][q4 * 4 + 2] = v.z; pw[h][q4 * 4 + 3] = v.w;
-                        }
-                    }
-                    // row above: neighbour lane's last row (this column), or the stripe boundary
-                    uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W);
-                    uint32_t upF = __shfl_up_sync(FULL, fLast, 1, W);
-                    if (L == 0) { upHO = bnd[u].x; upF = bnd[u].y; }
-                    uint32_t hd = prevUpHO;
-                    prevUpHO = upHO;
-                    uint32_t F = upF, hu = upHO;
-                    uint32_t H[K];
-#pragma unroll
-                    for (int r = 0; r < K; ++r) {
-                        uint32_t sc;
-                        if (NH == 2) {
-                            constexpr uint32_t SEL[4] = {0xC480u, 0xD591u, 0xE6A2u, 0xF7B3u};
-                            sc = prmt(pw[0][r >> 2], pw[1][r >> 2], SEL[r & 3]);
-                        } else {
-                            sc = pw[0][r];
-                        }
-                        st.E[r] = T::addmax(st.E[r], e2, st.HO[r]);
-                        F = T::addmax(F, e2, hu);
-                        const uint32_t tt = T::max_relu(st.E[r], F);
-                        const uint32_t h = T::addmax(hd, sc, tt);
-                        hd = st.HO[r];
-                        st.HO[r] = T::add(h, o2);
-                        hu = st.HO[r];
-                        H[r] = h;
-                    }
-                    hoLast = st.HO[K - 1];
-                    fLast = F;
-                    // running max over the lane's rows (strict improvement -> record column)
-                    uint32_t nb = best;
-#pragma unroll
-                    for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
-                    if (K & 1) nb = T::max2(nb, H[K - 1]);
-                    if (nb != best) {
-                        const uint32_t mask = T::changed_mask(nb, best);
-#pragma unroll
-                        for (int r = 0; r < K; ++r) st.SV[r] = (st.SV[r] & ~mask) | (st.HO[r] & mask);
-                        bestcol = (bestcol & ~mask) | (T::splat(t - L) & mask);
-                        best = nb;
-                        if (REV) {
-#pragma unroll
-                            for (int h = 0; h < NH; ++h) {
-                                if (h_pid[h] >= 0 && T::get(mask, h) != 0 && T::get(best, h) == h_tgt[h]) {
-                                    int rr = 0;
-#pragma unroll
-                                    for (int r = K - 1; r >= 0; --r) if (T::get(st.SV[r], h) == h_tgt[h] + o) rr = r;
-                                    const int j = t - L;
-                                    const int i = row0 + L * K + rr;
-                                    const unsigned long long key = ((unsigned long long)(uint32_t)h_tgt[h] << 32) |
-                                        ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
-                                    atomicMax(P.keys + h_pid[h], key);
-                                    atomicMin((int*)stop + seg * NH + h, j + W);
-                                }
-                            }
-                        }
-                    }
-                    if (!REV && t == next_ev) {
-#pragma unroll
-                        for (int h = 0; h < NH; ++h) {
-                            if (ev[h] == t) {
-                                const int b = T::get(best, h);
-                                if (b > 0) {
-                                    int rr = 0;
-#pragma unroll
-                                    for (int r = K - 1; r >= 0; --r) if (T::get(st.SV[r], h) == b + o) rr = r;
-                                    const int j = (NH == 2) ? (int)((bestcol >> (16 * h)) & 0xffff) : (int)bestcol;
-                                    const int i = row0 + L * K + rr;
-                                    const unsigned long long key = ((unsigned long long)(uint32_t)b << 32) |
-                                        ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
-                                    atomicMax(P.keys + h_pid[h], key);
-                                }
-                                best = T::set(best, h, T::FROZEN);
-                                ev[h] = 0x7fffffff;
-                            }
-                        }
-                        next_ev = ev[0];
-                        if (NH == 2) next_ev = min(next_ev, ev[NH - 1]);
-                    }
-                    if (to_scratch && L == W - 1) {
-                        const int c = t - (W - 1);
-                        if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-#pragma unroll
-                    for (int h = 0; h < NH; ++h) cd[u][h] = cdn[u][h];
-                    bnd[u] = bndn[u];
-                }
-                if (REV) {
-                    __syncwarp();
-                    int te = 0;
-#pragma unroll
-                    for (int sl = 0; sl < SLOTS; ++sl) {
-                        const int m_sl = __shfl_sync(FULL, s_m, sl);
-                        te = max(te, min(m_sl + W - 1, stop[sl]));
-                    }
-                    T_end = te;
-                }
+            // ---- the stripe's column sweep (single-stripe items skip all hand-off code) ----
+            if (ns == 1) {
+                sweep<T, W, K, REV, false>(P, prof, stop, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax, row0, o2, e2, o,
+                                           nullptr, nullptr, false, false);
+            } else {
+                const uint2* scr_in = reinterpret_cast<const uint2*>(
+                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes);
+                uint2* scr_out = reinterpret_cast<uint2*>(
+                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
+                sweep<T, W, K, REV, true>(P, prof, stop, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax, row0, o2, e2, o,
+                                          scr_in, scr_out, s > 0, s + 1 < ns);
             }
         }
     }

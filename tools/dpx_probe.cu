@@ -68,6 +68,35 @@ __global__ void probe(Out* out, unsigned seed, unsigned o2, unsigned e2) {
                 f[c] = (f[c] | h[c]) ^ e[c];
             } else if (V == 9) {
                 h[c] = __shfl_up_sync(0xffffffffu, h[c], 1, 16);
+            } else if (V == 10) {
+                h[c] = __vadd2(h[c], e[c]);
+            } else if (V == 11) {
+                h[c] = __viaddmax_s16x2(h[c], e2, e[c]);
+                x[c] = __vadd2(x[c], f[c]);
+            } else if (V == 12) {
+                // proposed cell: X = hd + s (VIADD), H = max3(X, E, F) relu, HO = H + o (VIADD), E, F addmax, PRMT, best/2
+                unsigned hd = x[c];
+                unsigned sc = prmt(hd, s, 0x3210 + (c & 3));
+                e[c] = __viaddmax_s16x2(e[c], e2, h[c]);
+                f[c] = __viaddmax_s16x2(f[c], e2, h[c]);
+                unsigned X = __vadd2(hd, sc);
+                unsigned H = __vimax3_s16x2_relu(X, e[c], f[c]);
+                x[c] = h[c];
+                h[c] = __vadd2(H, o2);
+                if (c & 1) best = __vimax3_s16x2_relu(best, H, h[c - 1]);
+            } else if (V == 13) {
+                // same without PRMT
+                unsigned hd = x[c];
+                e[c] = __viaddmax_s16x2(e[c], e2, h[c]);
+                f[c] = __viaddmax_s16x2(f[c], e2, h[c]);
+                unsigned X = __vadd2(hd, s);
+                unsigned H = __vimax3_s16x2_relu(X, e[c], f[c]);
+                x[c] = h[c];
+                h[c] = __vadd2(H, o2);
+                if (c & 1) best = __vimax3_s16x2_relu(best, H, h[c - 1]);
+            } else if (V == 14) {
+                h[c] = __viaddmax_s16x2(h[c], e2, e[c]);
+                x[c] = (x[c] != f[c]) ? x[c] : e[c];
             }
         }
     }
@@ -83,9 +112,10 @@ __global__ void probe(Out* out, unsigned seed, unsigned o2, unsigned e2) {
 }
 
 // instructions per chain-iteration (per thread) that the probe is meant to measure
-static const double INSTR_PER_CHAIN[10] = {5.5, 1, 1, 1, 1, 6.5, 5.5, 2, 2, 1};
-static const char* NAMES[10] = {"mix5.5(s16x2 gotoh)", "VIADDMNMX.S16x2", "VIMNMX3.S16x2(+LOP)", "PRMT", "IMAD",
-                                "mix+PRMT(6.5)", "mix,IMAD for H+o", "VIADDMNMX+IMAD", "LOP3 x2", "SHFL"};
+static const double INSTR_PER_CHAIN[15] = {5.5, 1, 1, 1, 1, 6.5, 5.5, 2, 2, 1, 1, 2, 6.5, 5.5, 3};
+static const char* NAMES[15] = {"mix5.5(s16x2 gotoh)", "VIADDMNMX.S16x2", "VIMNMX3.S16x2(+LOP)", "PRMT", "IMAD",
+                                "mix+PRMT(6.5)", "mix,IMAD for H+o", "VIADDMNMX+IMAD", "LOP3 x2", "SHFL",
+                                "VIADD.16x2", "VIADDMNMX+VIADD.16x2", "cell v2 +PRMT (6.5)", "cell v2 (5.5)", "VIADDMNMX+ISETP+SEL"};
 
 template <int V>
 void run(int sms, int blocks_per_sm, int threads) {
@@ -108,7 +138,7 @@ void run(int sms, int blocks_per_sm, int threads) {
     double mhz = (cyc / (ms * 1e-3)) / 1e6;
     printf("%-22s warps/SM=%2d  warp-instr/clk/SM=%.3f  GPU warp-instr/s=%.3e  implied SM MHz=%.0f  ms=%.3f\n",
            NAMES[V], warps_per_sm, ipc, wall_rate, mhz, ms);
-    if (V == 0 || V == 5 || V == 6) {
+    if (V == 0 || V == 5 || V == 6 || V == 12 || V == 13) {
         double cellpairs = (double)CHAINS * ITERS * 32.0 * warps;
         printf("    -> cell updates/s (2 cells per s16x2 chain step) = %.3f TCUPS\n", 2 * cellpairs / (ms * 1e-3) / 1e12);
     }
@@ -119,11 +149,12 @@ int main() {
     cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
     printf("device %s SMs=%d clockRate(kHz)=%d\n", p.name, p.multiProcessorCount, p.clockRate);
     int sms = p.multiProcessorCount;
-    for (int bps : {2, 4, 8}) {
+    for (int bps : {4, 8}) {
         printf("--- blocks/SM=%d x 256 threads\n", bps);
         run<0>(sms, bps, 256); run<1>(sms, bps, 256); run<2>(sms, bps, 256); run<3>(sms, bps, 256);
         run<4>(sms, bps, 256); run<5>(sms, bps, 256); run<6>(sms, bps, 256); run<7>(sms, bps, 256);
-        run<8>(sms, bps, 256); run<9>(sms, bps, 256);
+        run<8>(sms, bps, 256); run<9>(sms, bps, 256); run<10>(sms, bps, 256); run<11>(sms, bps, 256);
+        run<12>(sms, bps, 256); run<13>(sms, bps, 256); run<14>(sms, bps, 256);
     }
     return 0;
 }
