@@ -14,7 +14,7 @@ constexpr uint32_t FULL = 0xffffffffu;
 // bounds checks (the paper's "padding instead of boundary
 // checks" lesson, reused here).
 constexpr int PADL = 32;
-constexpr int PADR = 32;
+constexpr int PADR = 64;
 // Tail guard of the code buffers: a work item's shorter half keeps reading
 // (frozen, harmless) codes up to the item's longest reference + fill/drain.
 constexpr int64_t GUARD = SW_MAX_SEQ_LEN + 256;

@@ -69,9 +69,11 @@ struct Geometry {
     // profile bytes per (slot, code, lane): int8 x K (s16x2) or int32 x K (s32), 16 B aligned
     static constexpr int PB = (T::NH == 2) ? 16 * ((K + 15) / 16) : 16 * ((4 * K + 15) / 16);
     static constexpr int PWORDS = PB / 4;
+    static constexpr int SVB = 16 * ((4 * K + 15) / 16);    // saved improvement column per (lane, half)
     static __host__ __device__ int prof_bytes(int nc) { return SLOTS * nc * W * PB; }
-    // shared memory per warp: profile + REV stop steps
-    static __host__ __device__ int warp_smem(int nc) { return prof_bytes(nc) + 16 * ((SLOTS * 4 + 15) / 16); }
+    static constexpr int STOP_BYTES = 16 * ((SLOTS * 4 + 15) / 16);
+    // shared memory per warp: profile + REV stop steps + saved improvement columns
+    static __host__ __device__ int warp_smem(int nc) { return prof_bytes(nc) + STOP_BYTES + 32 * T::NH * SVB; }
 };
 
 template <class T, int K>
@@ -103,14 +105,54 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
     return v;
 }
 
+// Saved HO words of an improvement column, kept in shared memory (one slot
+// per lane and half; the full 32-bit words are stored, the half is picked at
+// read time).  Predicated STS.128 instead of per-row LOP3 merges keeps this
+// off the ALU pipe.
+template <int K>
+__device__ __forceinline__ void sv_store(uint32_t addr, const uint32_t (&HO)[K]) {
+#pragma unroll
+    for (int w = 0; w < (K + 3) / 4; ++w) {
+        const uint32_t a = HO[4 * w];
+        const uint32_t b = (4 * w + 1 < K) ? HO[4 * w + 1] : 0u;
+        const uint32_t c = (4 * w + 2 < K) ? HO[4 * w + 2] : 0u;
+        const uint32_t d = (4 * w + 3 < K) ? HO[4 * w + 3] : 0u;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr + 16 * w), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+    }
+}
+
+// First row r of the saved column whose half h equals `target` (an HO value).
+template <class T, int K>
+__device__ __forceinline__ int sv_first_row(uint32_t addr, int h, int target) {
+    int rr = 0;
+#pragma unroll
+    for (int w = (K + 3) / 4 - 1; w >= 0; --w) {
+        const uint4 v = lds128(addr + 16 * w);
+        const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int b = 3; b >= 0; --b)
+            if (4 * w + b < K && T::get(x[b], h) == target) rr = 4 * w + b;
+    }
+    return rr;
+}
+
+__device__ __forceinline__ unsigned long long pack_key(int S, int j, int i) {
+    return ((unsigned long long)(uint32_t)S << 32) | ((unsigned long long)(0xffff - j) << 16) |
+           (unsigned long long)(0xffff - i);
+}
+
 // One stripe of one work item: the column sweep of the anti-diagonal
 // wavefront for this lane's K rows of both halves.  MULTI adds the stripe
-// hand-off (boundary row in from scratch, bottom row out to scratch).
-template <class T, int W, int K, bool REV, bool MULTI>
-__device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const int seg,
-                                      const int L, const int s_m, const int (&h_pid)[T::NH], const int (&h_m)[T::NH],
-                                      const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH], const int mmax,
-                                      const int row0, const uint32_t o2, const uint32_t e2, const int o,
+// hand-off (boundary row in from scratch, bottom row out to scratch).  EV
+// (forward only) emits each half's result at its own last column; without EV
+// every half emits after the sweep, which is exact when the item's
+// references differ by at most the pad margin (the columns past a shorter
+// reference are pad codes, whose cells stay below S).
+template <class T, int W, int K, bool REV, bool MULTI, bool EV>
+__device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const uint32_t sv_base,
+                                      const int seg, const int L, const int s_m, const int (&h_pid)[T::NH],
+                                      const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
+                                      const int mmax, const int row0, const uint32_t o2, const uint32_t e2, const int o,
                                       const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
@@ -119,18 +161,22 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     constexpr int CS = W * G::PB;        // profile bytes per code
     const int nc = P.sc.nc;
 
-    uint32_t HO[K], E[K], SV[K];
+    uint32_t HO[K], E[K];
 #pragma unroll
-    for (int r = 0; r < K; ++r) { HO[r] = o2; E[r] = o2; SV[r] = 0; }
-    uint32_t best = 0, bestcol = 0;
-    uint32_t hoLast = o2, fLast = o2, prevUpHO = o2;
+    for (int r = 0; r < K; ++r) { HO[r] = o2; E[r] = o2; }
+    uint32_t best = 0;
+    int bc[NH];                          // column of the last strict improvement, per half
+    uint32_t sv[NH];                     // shared address of the half's saved column
     int ev[NH];
     int next_ev = 0x7fffffff;
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
-        ev[h] = (!REV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
+        bc[h] = 0;
+        sv[h] = sv_base + (uint32_t)h * G::SVB;
+        ev[h] = (EV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
         next_ev = min(next_ev, ev[h]);
     }
+    uint32_t hoLast = o2, fLast = o2, prevUpHO = o2;
     uint32_t prof_h[NH];  // shared-window address of this lane's profile entries, code 0
     const uint8_t* rp[NH];
 #pragma unroll
@@ -143,6 +189,14 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     const uint32_t notL0 = opaque(L != 0 ? 1u : 0u);
     const uint32_t b0 = (L == 0) ? o2 : 0u;
 
+    auto emit = [&](int h) {  // forward result of half h for this lane and stripe
+        const int b = T::get(best, h);
+        if (h_pid[h] >= 0 && b > 0) {
+            const int rr = sv_first_row<T, K>(sv[h], h, b + o);
+            atomicMax(P.keys + h_pid[h], pack_key(b, bc[h], row0 + L * K + rr));
+        }
+    };
+
     // rotating prefetch of the next U columns' codes (and boundary rows)
     uint32_t cd[U][NH];
     uint2 bnd[U];
@@ -150,7 +204,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     for (int u = 0; u < U; ++u) {
 #pragma unroll
         for (int h = 0; h < NH; ++h) cd[u][h] = ld_code(rp[h] + u);
-        if (MULTI) bnd[u] = (from_scratch && L == 0) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
+        if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
     }
 
     int T_end = mmax + W - 1;
@@ -180,7 +234,9 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
             uint32_t bHO = b0, bF = b0;
             if (MULTI) {
                 bHO = bnd[u].x; bF = bnd[u].y;
-                bnd[u] = (from_scratch && L == 0) ? __ldcg(scr_in + t + U) : make_uint2(b0, b0);
+                // columns past the item's longest reference were never handed off: they take
+                // the constant boundary, so pad-column cells stay below S (see EV above)
+                bnd[u] = (from_scratch && L == 0 && t + U < mmax) ? __ldcg(scr_in + t + U) : make_uint2(b0, b0);
             }
             // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
             const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
@@ -215,43 +271,31 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
             for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
             if (K & 1) nb = T::max2(nb, H[K - 1]);
             if (nb != best) {
-                const uint32_t mask = T::changed_mask(nb, best);
+                const uint32_t d = nb ^ best;
 #pragma unroll
-                for (int r = 0; r < K; ++r) SV[r] = (SV[r] & ~mask) | (HO[r] & mask);
-                bestcol = (bestcol & ~mask) | (T::splat(t - L) & mask);
-                best = nb;
-                if (REV) {
+                for (int h = 0; h < NH; ++h) {
+                    if (NH == 1 || ((d >> (16 * h)) & 0xffffu)) {
+                        bc[h] = t - L;
+                        if (REV) {
+                            if (h_pid[h] >= 0 && T::get(nb, h) == h_tgt[h]) {
+                                int rr = 0;
 #pragma unroll
-                    for (int h = 0; h < NH; ++h) {
-                        if (h_pid[h] >= 0 && T::get(mask, h) != 0 && T::get(best, h) == h_tgt[h]) {
-                            int rr = 0;
-#pragma unroll
-                            for (int r = K - 1; r >= 0; --r) if (T::get(SV[r], h) == h_tgt[h] + o) rr = r;
-                            const int j = t - L;
-                            const int i = row0 + L * K + rr;
-                            const unsigned long long key = ((unsigned long long)(uint32_t)h_tgt[h] << 32) |
-                                ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
-                            atomicMax(P.keys + h_pid[h], key);
-                            atomicMin((int*)stop + seg * NH + h, j + W);
+                                for (int r = K - 1; r >= 0; --r) if (T::get(HO[r], h) == h_tgt[h] + o) rr = r;
+                                atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
+                                atomicMin((int*)stop + seg * NH + h, t - L + W);
+                            }
+                        } else {
+                            sv_store<K>(sv[h], HO);
                         }
                     }
                 }
+                best = nb;
             }
-            if (!REV && t == next_ev) {
+            if (EV && t == next_ev) {
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     if (ev[h] == t) {
-                        const int b = T::get(best, h);
-                        if (b > 0) {
-                            int rr = 0;
-#pragma unroll
-                            for (int r = K - 1; r >= 0; --r) if (T::get(SV[r], h) == b + o) rr = r;
-                            const int j = (NH == 2) ? (int)((bestcol >> (16 * h)) & 0xffff) : (int)bestcol;
-                            const int i = row0 + L * K + rr;
-                            const unsigned long long key = ((unsigned long long)(uint32_t)b << 32) |
-                                ((unsigned long long)(0xffff - j) << 16) | (unsigned long long)(0xffff - i);
-                            atomicMax(P.keys + h_pid[h], key);
-                        }
+                        emit(h);
                         best = T::set(best, h, T::FROZEN);
                         ev[h] = 0x7fffffff;
                     }
@@ -272,8 +316,11 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
             T_end = te;
         }
     }
+    if (!REV && !EV) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) emit(h);
+    }
 }
-
 
 template <class T, int W, int K, bool REV>
 __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
@@ -289,6 +336,8 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
     const int nc = P.sc.nc;
     uint8_t* prof = smem + (size_t)warp * G::warp_smem(nc);
     volatile int* stop = reinterpret_cast<volatile int*>(prof + G::prof_bytes(nc));
+    const uint32_t sv_base = (uint32_t)__cvta_generic_to_shared(prof + G::prof_bytes(nc) + G::STOP_BYTES) +
+                             (uint32_t)(lane * NH * G::SVB);
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
     const int n_path = *P.count;
@@ -318,12 +367,16 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
                 if (REV) s_tgt = P.target[s_pid];
             }
         }
-        int mmax = s_m, nmax = s_n;
+        int mmax = s_m, nmax = s_n, mmin = s_pid >= 0 ? s_m : 0x7fffffff;
 #pragma unroll
         for (int d = 16; d >= 1; d >>= 1) {
             mmax = max(mmax, __shfl_xor_sync(FULL, mmax, d));
             nmax = max(nmax, __shfl_xor_sync(FULL, nmax, d));
+            mmin = min(mmin, __shfl_xor_sync(FULL, mmin, d));
         }
+        // per-half end events are needed only when a shorter reference of the item runs
+        // out of pad codes before the sweep ends (see sweep<>, EV)
+        const bool need_ev = !REV && (mmax - mmin > PADR - W - 8);
         const int ns = (nmax + G::ROWS - 1) / G::ROWS;
 
         // this lane's halves
@@ -394,15 +447,23 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
 
             // ---- the stripe's column sweep (single-stripe items skip all hand-off code) ----
             if (ns == 1) {
-                sweep<T, W, K, REV, false>(P, prof, stop, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax, row0, o2, e2, o,
-                                           nullptr, nullptr, false, false);
+                if (need_ev)
+                    sweep<T, W, K, REV, false, true>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                     row0, o2, e2, o, nullptr, nullptr, false, false);
+                else
+                    sweep<T, W, K, REV, false, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
             } else {
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes);
                 uint2* scr_out = reinterpret_cast<uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
-                sweep<T, W, K, REV, true>(P, prof, stop, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax, row0, o2, e2, o,
-                                          scr_in, scr_out, s > 0, s + 1 < ns);
+                if (need_ev)
+                    sweep<T, W, K, REV, true, true>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                    row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
+                else
+                    sweep<T, W, K, REV, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
             }
         }
     }
