@@ -49,7 +49,7 @@ struct sw_context {
 
     // per-pair
     DevBuf<int32_t> nlen, mlen, nlen_rev, mlen_rev, target, iota, order, order_rev;
-    DevBuf<int64_t> rpos;
+    DevBuf<int64_t> qpos, rpos;
     DevBuf<uint8_t> flags;
     DevBuf<uint32_t> key, key_sorted;
     DevBuf<unsigned long long> keys_fwd, keys_rev;
@@ -221,14 +221,17 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
     }
     const size_t tq = (size_t)(qN - q0), tr = (size_t)(rN - r0);
-    const size_t rbytes = tr + N * (PADL + PADR) + GUARD;
+    const size_t rbytes = tr + N * (PADL + PADR) + GUARD + 16;
+    // code buffers keep the payloads' 16-byte phase so pack moves aligned vectors
+    const int64_t qshift = (int64_t)(((uintptr_t)(queries + q0)) & 15);
+    const int64_t rshift = (int64_t)(((uintptr_t)(refs + r0)) & 15);
 
     // 2. workspace
 #define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
     ENS(nlen, N); ENS(mlen, N); ENS(nlen_rev, N); ENS(mlen_rev, N); ENS(target, N); ENS(iota, N);
-    ENS(order, N); ENS(order_rev, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
+    ENS(order, N); ENS(order_rev, N); ENS(qpos, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
     ENS(keys_fwd, N); ENS(keys_rev, N);
-    ENS(qcode, tq + 16); ENS(qrev, tq + 16);
+    ENS(qcode, tq + 32); ENS(qrev, tq + 32);
     {
         // Every byte of the reference code buffers must be a valid code of the batch's
         // alphabet: finished halves of a work item keep reading past their reference.
@@ -255,11 +258,11 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     {
         PackParams P;
         P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.n_pairs = n_pairs;
-        P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN;
+        P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
         P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma;
         P.rows_s16 = rows16; P.rows_s32 = rows32;
         P.qcode = h->qcode.p; P.rcode = h->rcode.p; P.rrev = h->rrev.p;
-        P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
+        P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
         P.iota = h->iota.p; P.stats = h->d_stats;
         const int64_t warps = std::min<int64_t>(n_pairs, (int64_t)h->sm_count * 64);
         const int blocks = (int)((warps * 32 + 255) / 256);
@@ -316,7 +319,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     // 6. forward wavefront
     SW_CUDA(h, cudaMemsetAsync(h->d_counters, 0, 4 * sizeof(int32_t), s));
     WaveParams W;
-    W.q_off = q_off; W.q0 = q0; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.sc = sc;
+    W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.sc = sc;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p;
     W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &h->d_stats->swept_fwd;
     if (lf16.blocks > 0) {
@@ -337,7 +340,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     FinishParams F;
     F.n_pairs = n_pairs; F.flags = h->flags.p; F.keys_fwd = h->keys_fwd.p; F.keys_rev = h->keys_rev.p;
     F.qcode = h->qcode.p; F.qrev = h->qrev.p; F.rcode = h->rcode.p; F.rrev = h->rrev.p;
-    F.q_off = q_off; F.q0 = q0; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
+    F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
     F.target = h->target.p; F.key_rev = h->key.p; F.iota = h->iota.p; F.rows_s16 = rows16; F.rows_s32 = rows32;
     F.out = *out; F.stats = h->d_stats;
     {
@@ -503,7 +506,7 @@ sw_status_t sw_free(sw_handle_t h) {
     if (h->have_last) cudaStreamSynchronize(h->last_stream);
     cudaDeviceSynchronize();
     release(h->nlen); release(h->mlen); release(h->nlen_rev); release(h->mlen_rev); release(h->target);
-    release(h->iota); release(h->order); release(h->order_rev); release(h->rpos); release(h->flags);
+    release(h->iota); release(h->order); release(h->order_rev); release(h->qpos); release(h->rpos); release(h->flags);
     release(h->key); release(h->key_sorted); release(h->keys_fwd); release(h->keys_rev);
     release(h->qcode); release(h->qrev); release(h->rcode); release(h->rrev); release(h->cub_temp);
     release(h->scratch); release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);

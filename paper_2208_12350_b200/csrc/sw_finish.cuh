@@ -16,8 +16,7 @@ struct FinishParams {
     uint8_t* qrev;
     const uint8_t* rcode;
     uint8_t* rrev;
-    const int64_t* q_off;
-    int64_t q0;
+    const int64_t* qpos;
     const int64_t* rpos;
     int32_t* nlen_rev;
     int32_t* mlen_rev;
@@ -68,7 +67,7 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
             }
             continue;
         }
-        const int64_t qp = P.q_off[p] - P.q0;
+        const int64_t qp = P.qpos[p];
         const int64_t rp = P.rpos[p];
         for (int k = lane; k <= i; k += 32) P.qrev[qp + k] = P.qcode[qp + i - k];
         for (int k = lane; k <= j; k += 32) P.rrev[rp + k] = P.rcode[rp + j - k];
@@ -81,7 +80,9 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
             P.nlen_rev[p] = n2;
             P.mlen_rev[p] = m2;
             P.target[p] = S;
-            P.key_rev[p] = (s16 ? KEY_S16 : KEY_S32) | (stripes << 16) | (uint32_t)m2;
+            // reverse work items are grouped by S: the early-stopped sweep's length follows the
+            // alignment's span, for which S is the available proxy
+            P.key_rev[p] = (s16 ? KEY_S16 : KEY_S32) | (stripes << 16) | (uint32_t)min(S, 0xffff);
             P.iota[p] = (int32_t)p;
             if (s16) ++l16; else ++l32;
         }

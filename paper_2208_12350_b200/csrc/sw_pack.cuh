@@ -30,6 +30,7 @@ struct PackParams {
     const int64_t* r_off;
     int64_t n_pairs;
     int64_t q0, qN, r0, rN;      // payload extents (host-read)
+    int64_t qshift, rshift;      // (payload + extent start) mod 16: code buffers keep the payload's alignment
     int alphabet;
     int s16_ok;                  // scoring fits the s16x2 path (int8 profile, int16 range)
     int max_sigma;
@@ -39,6 +40,7 @@ struct PackParams {
     uint8_t* rrev;               // padded layout (pads only here)
     int32_t* nlen;
     int32_t* mlen;
+    int64_t* qpos;
     int64_t* rpos;
     uint8_t* flags;
     uint32_t* key;
@@ -46,37 +48,83 @@ struct PackParams {
     BatchStats* stats;
 };
 
-// ASCII -> code, case-insensitive; CODE_BAD outside the alphabet (reading R10).
-__device__ __forceinline__ uint8_t dna_code(uint8_t ch) {
-    ch &= 0xdf;  // upper-case letters (non-letters stay invalid below)
-    switch (ch) {
-        case 'A': return 0;
-        case 'C': return 1;
-        case 'G': return 2;
-        case 'T': return 3;
-        default: return CODE_BAD;
-    }
-}
-
-__device__ __forceinline__ uint8_t protein_code(uint8_t ch) {
-    if (ch == '*') return 23;
+// ASCII -> code table, case-insensitive; CODE_BAD outside the alphabet (reading R10).
+__device__ __forceinline__ uint8_t ascii_code(int alphabet, int ch) {
     if (ch >= 'a' && ch <= 'z') ch -= 32;
-    // A R N D C Q E G H I L K M F P S T W Y V B Z X
+    if (alphabet == SW_ALPHABET_DNA) {
+        switch (ch) {
+            case 'A': return 0;
+            case 'C': return 1;
+            case 'G': return 2;
+            case 'T': return 3;
+            default: return CODE_BAD;
+        }
+    }
+    // A R N D C Q E G H I L K M F P S T W Y V B Z X *
     switch (ch) {
         case 'A': return 0;  case 'R': return 1;  case 'N': return 2;  case 'D': return 3;
         case 'C': return 4;  case 'Q': return 5;  case 'E': return 6;  case 'G': return 7;
         case 'H': return 8;  case 'I': return 9;  case 'L': return 10; case 'K': return 11;
         case 'M': return 12; case 'F': return 13; case 'P': return 14; case 'S': return 15;
         case 'T': return 16; case 'W': return 17; case 'Y': return 18; case 'V': return 19;
-        case 'B': return 20; case 'Z': return 21; case 'X': return 22;
+        case 'B': return 20; case 'Z': return 21; case 'X': return 22; case '*': return 23;
         default: return CODE_BAD;
     }
+}
+
+__device__ __forceinline__ uint32_t conv4(uint32_t w, const uint8_t* lut, uint32_t& badmask) {
+    const uint32_t c0 = lut[w & 0xff], c1 = lut[(w >> 8) & 0xff], c2 = lut[(w >> 16) & 0xff], c3 = lut[w >> 24];
+    badmask |= c0 | c1 | c2 | c3;  // CODE_BAD has bit 7 set, valid codes do not
+    return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
+}
+
+// Convert one sequence: src and dst have the same address mod 16 (by construction of
+// the code-buffer positions), so the body moves as aligned 16-byte vectors.
+// Returns true if a symbol is outside the alphabet; such symbols become `bad_to`.
+__device__ __forceinline__ bool convert_run(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t len,
+                                            const uint8_t* lut, uint8_t bad_to, int lane) {
+    uint32_t badmask = 0;
+    bool bad = false;
+    const int head = (int)(len < (int64_t)((16 - ((uintptr_t)src & 15)) & 15) ? len : (int64_t)((16 - ((uintptr_t)src & 15)) & 15));
+    if (lane < head) {
+        const uint8_t c = lut[src[lane]];
+        bad |= c == CODE_BAD;
+        dst[lane] = c == CODE_BAD ? bad_to : c;
+    }
+    const int64_t body = (len - head) >> 4;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (int64_t k = lane; k < body; k += 32) {
+        const uint4 v = __ldg(s4 + k);
+        uint32_t bm = 0;
+        uint4 o;
+        o.x = conv4(v.x, lut, bm); o.y = conv4(v.y, lut, bm); o.z = conv4(v.z, lut, bm); o.w = conv4(v.w, lut, bm);
+        if (bm & 0x80u) {  // rare: replace bad bytes
+            uint32_t* ow = &o.x;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if (((ow[q] >> (8 * b)) & 0xff) == CODE_BAD) ow[q] = (ow[q] & ~(0xffu << (8 * b))) | ((uint32_t)bad_to << (8 * b));
+        }
+        badmask |= bm;
+        d4[k] = o;
+    }
+    const int64_t t0 = head + body * 16;
+    if (lane < len - t0) {
+        const uint8_t c = lut[src[t0 + lane]];
+        bad |= c == CODE_BAD;
+        dst[t0 + lane] = c == CODE_BAD ? bad_to : c;
+    }
+    return bad || (badmask & 0x80u);
 }
 
 __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
     __shared__ int s_bad, s_s16, s_s32, s_maxn, s_maxm, s_malformed;
     __shared__ unsigned long long s_cells;
+    __shared__ uint8_t lut[256];
     if (threadIdx.x == 0) { s_bad = s_s16 = s_s32 = s_maxn = s_maxm = s_malformed = 0; s_cells = 0; }
+    for (int c = threadIdx.x; c < 256; c += blockDim.x) lut[c] = ascii_code(P.alphabet, c);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -91,22 +139,14 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
         bool in_range = qa >= P.q0 && qb <= P.qN && ra >= P.r0 && rb <= P.rN && n >= 0 && m >= 0;
         if (n < 0 || m < 0) l_malf = 1;
         bool bad = !in_range || n > SW_MAX_SEQ_LEN || m > SW_MAX_SEQ_LEN;
-        const int64_t rp = (ra - P.r0) + (p + 1) * PADL + p * PADR;
-        if (in_range) {
-            const int64_t qp = qa - P.q0;
-            for (int64_t i = lane; i < n; i += 32) {
-                uint8_t c = P.alphabet == SW_ALPHABET_DNA ? dna_code(P.queries[qa + i]) : protein_code(P.queries[qa + i]);
-                bad |= (c == CODE_BAD);
-                P.qcode[qp + i] = c;
-            }
-            for (int64_t j = lane; j < m; j += 32) {
-                uint8_t c = P.alphabet == SW_ALPHABET_DNA ? dna_code(P.refs[ra + j]) : protein_code(P.refs[ra + j]);
-                bad |= (c == CODE_BAD);
-                P.rcode[rp + j] = (c == CODE_BAD) ? pad_code : c;  // the wavefront indexes the profile by code
-            }
+        const int64_t qp = (qa - P.q0) + P.qshift;
+        const int64_t rp = (ra - P.r0) + (p + 1) * PADL + p * PADR + P.rshift;
+        if (in_range && !bad) {
+            bad |= convert_run(P.queries + qa, P.qcode + qp, n, lut, pad_code, lane);
+            bad |= convert_run(P.refs + ra, P.rcode + rp, m, lut, pad_code, lane);
             // pads around the reference, in both the forward and the reverse buffer
             for (int k = lane; k < PADL + PADR; k += 32) {
-                int64_t pos = k < PADL ? rp - PADL + k : rp + m + (k - PADL);
+                const int64_t pos = k < PADL ? rp - PADL + k : rp + m + (k - PADL);
                 P.rcode[pos] = pad_code;
                 P.rrev[pos] = pad_code;
             }
@@ -135,6 +175,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
             }
             P.nlen[p] = nn;
             P.mlen[p] = mm;
+            P.qpos[p] = qp;
             P.rpos[p] = rp;
             P.flags[p] = fl;
             P.key[p] = key;

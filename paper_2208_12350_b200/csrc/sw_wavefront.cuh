@@ -42,11 +42,10 @@
 namespace swb {
 
 struct WaveParams {
-    const uint8_t* qcode;       // query codes (positions q_off[p] - q0)
+    const uint8_t* qcode;       // query codes (positions qpos[p])
     const uint8_t* rcode;       // reference codes (padded positions rpos[p])
-    const int64_t* q_off;       // caller offsets (device)
-    int64_t q0;
-    const int64_t* rpos;
+    const int64_t* qpos;        // query code position per pair
+    const int64_t* rpos;        // reference code position per pair
     const int32_t* nlen;        // rows of each pair (forward: n, reverse: q_end+1)
     const int32_t* mlen;        // columns (forward: m, reverse: r_end+1)
     const int32_t* order;       // pair ids sorted by work key
@@ -363,7 +362,7 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
                 s_n = P.nlen[s_pid];
                 s_m = P.mlen[s_pid];
                 s_rpos = P.rpos[s_pid];
-                s_qpos = P.q_off[s_pid] - P.q0;
+                s_qpos = P.qpos[s_pid];
                 if (REV) s_tgt = P.target[s_pid];
             }
         }
