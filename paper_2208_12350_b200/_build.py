@@ -31,21 +31,24 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile libsw_b200.so.  `out`/`defines` build a variant elsewhere (tuning experiments)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    tmp = target + f".tmp{os.getpid()}"
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC,
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(PKG, "build.log")
+    log = target + ".build.log" if out else os.path.join(PKG, "build.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed (see {log}):\n{res.stderr[-4000:]}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     if verbose:
         print(res.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

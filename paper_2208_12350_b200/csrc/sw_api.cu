@@ -60,7 +60,7 @@ struct sw_context {
     BatchStats* d_stats = nullptr;
     BatchStats* h_stats = nullptr;
     int64_t* h_ext = nullptr;
-    int32_t* d_counters = nullptr;  // 4 item counters
+    int32_t* d_counters = nullptr;  // work-queue heads: 3 forward + 3 reverse routes
     uint32_t* d_sink = nullptr;
     // host-buffer entry point staging
     DevBuf<uint8_t> st_q, st_r;
@@ -259,7 +259,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         PackParams P;
         P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.n_pairs = n_pairs;
         P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
-        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma;
+        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = K16 <= 16 ? 1 : 0;
         P.rows_s16 = rows16; P.rows_s32 = rows32;
         P.qcode = h->qcode.p; P.rcode = h->rcode.p; P.rrev = h->rrev.p;
         P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
@@ -281,27 +281,37 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     }
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[2], s));
 
-    auto kf16 = wavefront_kernel<TS16, W16, K16, false>;
-    auto kr16 = wavefront_kernel<TS16, W16, K16, true>;
-    auto kf32 = wavefront_kernel<TS32, W32, K32, false>;
-    auto kr32 = wavefront_kernel<TS32, W32, K32, true>;
-    const Launch lf16 = plan_wave<G16>(h, (const void*)kf16, sc.nc, hs.n_s16);
-    const Launch lr16 = plan_wave<G16>(h, (const void*)kr16, sc.nc, hs.n_s16);
-    const Launch lf32 = plan_wave<G32>(h, (const void*)kf32, sc.nc, hs.n_s32);
-    const Launch lr32 = plan_wave<G32>(h, (const void*)kr32, sc.nc, hs.n_s32);
+    // one kernel per route and pass (routes: TAG, S16, S32; sw_common.cuh)
+    const void* kfwd[N_ROUTES] = {(const void*)wavefront_kernel<TS16, W16, K16, false, true>,
+                                  (const void*)wavefront_kernel<TS16, W16, K16, false, false>,
+                                  (const void*)wavefront_kernel<TS32, W32, K32, false, false>};
+    const void* krev[N_ROUTES] = {(const void*)wavefront_kernel<TS16, W16, K16, true, true>,
+                                  (const void*)wavefront_kernel<TS16, W16, K16, true, false>,
+                                  (const void*)wavefront_kernel<TS32, W32, K32, true, false>};
+    Launch lf[N_ROUTES], lr[N_ROUTES];
+    for (int r = 0; r < N_ROUTES; ++r) {
+        // reverse-pass pairs are a subset of the forward ones: forward counts bound the grids
+        if (r == ROUTE_S32) {
+            lf[r] = plan_wave<G32>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
+            lr[r] = plan_wave<G32>(h, krev[r], sc.nc, hs.fwd_count[r]);
+        } else {
+            lf[r] = plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
+            lr[r] = plan_wave<G16>(h, krev[r], sc.nc, hs.fwd_count[r]);
+        }
+    }
 
     // stripe hand-off scratch: only if some query spans more than one stripe
-    int64_t seg16 = 0, seg32 = 0;
+    int64_t seg_bytes = 0;
     {
         size_t need = 0;
         const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16) * 8;
-        if (hs.n_s16 && hs.max_n > rows16) {
-            seg16 = row_bytes;
-            need = std::max(need, (size_t)std::max(lf16.blocks, lr16.blocks) * WARPS_PER_BLOCK * G16::SEGS * 2 * seg16);
-        }
-        if (hs.n_s32 && hs.max_n > rows32) {
-            seg32 = row_bytes;
-            need = std::max(need, (size_t)std::max(lf32.blocks, lr32.blocks) * WARPS_PER_BLOCK * G32::SEGS * 2 * seg32);
+        for (int r = 0; r < N_ROUTES; ++r) {
+            const int rows = r == ROUTE_S32 ? rows32 : rows16;
+            const int segs = r == ROUTE_S32 ? G32::SEGS : G16::SEGS;
+            if (hs.fwd_count[r] && hs.max_n > rows) {
+                seg_bytes = row_bytes;
+                need = std::max(need, (size_t)std::max(lf[r].blocks, lr[r].blocks) * WARPS_PER_BLOCK * segs * 2 * row_bytes);
+            }
         }
         if (need) ENS(scratch, need);
     }
@@ -317,21 +327,18 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[3], s));
 
     // 6. forward wavefront
-    SW_CUDA(h, cudaMemsetAsync(h->d_counters, 0, 4 * sizeof(int32_t), s));
+    SW_CUDA(h, cudaMemsetAsync(h->d_counters, 0, 8 * sizeof(int32_t), s));
     WaveParams W;
-    W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.sc = sc;
+    W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
+    W.tag_mul = 64;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p;
-    W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &h->d_stats->swept_fwd;
-    if (lf16.blocks > 0) {
-        W.count = &h->d_stats->n_s16; W.first = nullptr; W.item_counter = h->d_counters + 0; W.scratch_seg_bytes = seg16;
-        kf16<<<lf16.blocks, THREADS, lf16.smem, s>>>(W);
-        SW_CUDA(h, cudaGetLastError());
-        ++h->own_launches;
-    }
-    if (lf32.blocks > 0) {
-        W.count = &h->d_stats->n_s32; W.first = &h->d_stats->n_s16; W.item_counter = h->d_counters + 1; W.scratch_seg_bytes = seg32;
-        kf32<<<lf32.blocks, THREADS, lf32.smem, s>>>(W);
-        SW_CUDA(h, cudaGetLastError());
+    W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &h->d_stats->swept_fwd; W.counts = h->d_stats->fwd_count;
+    for (int r = 0; r < N_ROUTES; ++r) {
+        if (lf[r].blocks <= 0) continue;
+        W.route = r;
+        W.item_counter = h->d_counters + r;
+        void* args[] = {&W};
+        SW_CUDA(h, cudaLaunchKernel(kfwd[r], dim3(lf[r].blocks), dim3(THREADS), args, (size_t)lf[r].smem, s));
         ++h->own_launches;
     }
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[4], s));
@@ -360,17 +367,13 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
 
     // 8. reverse wavefront on the reversed prefixes
     W.qcode = h->qrev.p; W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p;
-    W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &h->d_stats->swept_rev;
-    if (lr16.blocks > 0) {
-        W.count = &h->d_stats->n_rev_s16; W.first = nullptr; W.item_counter = h->d_counters + 2; W.scratch_seg_bytes = seg16;
-        kr16<<<lr16.blocks, THREADS, lr16.smem, s>>>(W);
-        SW_CUDA(h, cudaGetLastError());
-        ++h->own_launches;
-    }
-    if (lr32.blocks > 0) {
-        W.count = &h->d_stats->n_rev_s32; W.first = &h->d_stats->n_rev_s16; W.item_counter = h->d_counters + 3; W.scratch_seg_bytes = seg32;
-        kr32<<<lr32.blocks, THREADS, lr32.smem, s>>>(W);
-        SW_CUDA(h, cudaGetLastError());
+    W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &h->d_stats->swept_rev; W.counts = h->d_stats->rev_count;
+    for (int r = 0; r < N_ROUTES; ++r) {
+        if (lr[r].blocks <= 0) continue;
+        W.route = r;
+        W.item_counter = h->d_counters + 4 + r;
+        void* args[] = {&W};
+        SW_CUDA(h, cudaLaunchKernel(krev[r], dim3(lr[r].blocks), dim3(THREADS), args, (size_t)lr[r].smem, s));
         ++h->own_launches;
     }
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[6], s));
@@ -425,14 +428,16 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
     h->sm_count = p.multiProcessorCount;
     // opt in to large dynamic shared memory (protein profiles)
     const int big = 200 * 1024;
-    set_smem_attr(wavefront_kernel<TS16, W16, K16, false>, big);
-    set_smem_attr(wavefront_kernel<TS16, W16, K16, true>, big);
-    set_smem_attr(wavefront_kernel<TS32, W32, K32, false>, big);
-    set_smem_attr(wavefront_kernel<TS32, W32, K32, true>, big);
+    set_smem_attr(wavefront_kernel<TS16, W16, K16, false, true>, big);
+    set_smem_attr(wavefront_kernel<TS16, W16, K16, true, true>, big);
+    set_smem_attr(wavefront_kernel<TS16, W16, K16, false, false>, big);
+    set_smem_attr(wavefront_kernel<TS16, W16, K16, true, false>, big);
+    set_smem_attr(wavefront_kernel<TS32, W32, K32, false, false>, big);
+    set_smem_attr(wavefront_kernel<TS32, W32, K32, true, false>, big);
     if (cudaMalloc(&h->d_stats, sizeof(BatchStats)) != cudaSuccess ||
         cudaMallocHost(&h->h_stats, sizeof(BatchStats)) != cudaSuccess ||
         cudaMallocHost(&h->h_ext, 4 * sizeof(int64_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_counters, 4 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_counters, 8 * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess) {
         sw_free(h);
         return SW_ERR_OUT_OF_MEMORY;

@@ -23,13 +23,20 @@ constexpr int NC_DNA = 5;        // A C G T + pad
 constexpr int NC_PROTEIN = 25;   // 24 BLOSUM62 symbols + pad
 constexpr uint8_t CODE_BAD = 0xff;
 
-// Forward/reverse work keys: [31] s16x2 path, [30] s32 path, [29:16] stripes, [15:0] m
-constexpr uint32_t KEY_S16 = 1u << 31;
-constexpr uint32_t KEY_S32 = 1u << 30;
+// Kernel routes of a pair:
+//   ROUTE_TAG  s16x2 lanes, column-in-block and row carried in the low 6 bits of the running max
+//              (pairs whose largest possible score is <= TAG_MAX_SCORE)
+//   ROUTE_S16  s16x2 lanes, improvement columns saved to shared memory
+//   ROUTE_S32  int32 lanes (scorings / lengths that are not int16-safe)
+constexpr int ROUTE_TAG = 0, ROUTE_S16 = 1, ROUTE_S32 = 2, N_ROUTES = 3;
+constexpr int TAG_MAX_SCORE = 511;    // 511 * 64 + 63 < 32768 (6 tag bits: column-in-block, row)
+// Work keys: [31:30] 3 - route (0 = trivial / invalid), [29:16] stripes, [15:0] columns
+__host__ __device__ constexpr uint32_t route_key(int route) { return (uint32_t)(3 - route) << 30; }
 
-// per-pair flags
+// per-pair flags: bit 0 invalid, bits 2:1 route
 constexpr uint8_t FLAG_BAD = 1;
-constexpr uint8_t FLAG_S16 = 2;
+__host__ __device__ constexpr uint8_t route_flag(int route) { return (uint8_t)(route << 1); }
+__host__ __device__ constexpr int flag_route(uint8_t f) { return (f >> 1) & 3; }
 
 // Product copy of NCBI BLOSUM62 (order ARNDCQEGHILKMFPSTWYVBZX*), R11.
 __constant__ int8_t c_blosum62[24][24] = {
@@ -96,6 +103,8 @@ struct TS16 {
     // max(a + b, c)
     static __device__ __forceinline__ V addmax(V a, V b, V c) { return __viaddmax_s16x2(a, b, c); }
     static __device__ __forceinline__ V max_relu(V a, V b) { return __vimax_s16x2_relu(a, b); }
+    // max(a + b, c, 0)
+    static __device__ __forceinline__ V addmax_relu(V a, V b, V c) { return __viaddmax_s16x2_relu(a, b, c); }
     static __device__ __forceinline__ V max3(V a, V b, V c) { return __vimax3_s16x2_relu(a, b, c); }
     static __device__ __forceinline__ V max2(V a, V b) { return __vimax_s16x2_relu(a, b); }
     // per-half all-ones mask where a != b (a >= b per half guaranteed)
@@ -118,6 +127,7 @@ struct TS32 {
     static __device__ __forceinline__ V add(V a, V b) { return (uint32_t)((int)a + (int)b); }
     static __device__ __forceinline__ V addmax(V a, V b, V c) { return (uint32_t)__viaddmax_s32((int)a, (int)b, (int)c); }
     static __device__ __forceinline__ V max_relu(V a, V b) { return (uint32_t)__vimax_s32_relu((int)a, (int)b); }
+    static __device__ __forceinline__ V addmax_relu(V a, V b, V c) { return (uint32_t)__viaddmax_s32_relu((int)a, (int)b, (int)c); }
     static __device__ __forceinline__ V max3(V a, V b, V c) { return (uint32_t)__vimax3_s32_relu((int)a, (int)b, (int)c); }
     static __device__ __forceinline__ V max2(V a, V b) { return (uint32_t)__vimax_s32_relu((int)a, (int)b); }
     static __device__ __forceinline__ V changed_mask(V newv, V oldv) { return newv != oldv ? 0xffffffffu : 0u; }

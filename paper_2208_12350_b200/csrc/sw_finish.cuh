@@ -39,13 +39,13 @@ __device__ __forceinline__ void decode_key(unsigned long long key, int& S, int& 
 // reverse(q[0..q_end]) x reverse(r[0..r_end]) materialised for the reverse
 // pass (reading R6).  One warp per pair.
 __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
-    __shared__ int s_r16, s_r32;
-    if (threadIdx.x == 0) { s_r16 = s_r32 = 0; }
+    __shared__ int s_route[N_ROUTES];
+    if (threadIdx.x < N_ROUTES) s_route[threadIdx.x] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    int l16 = 0, l32 = 0;
+    int l_route[N_ROUTES] = {0, 0, 0};
     for (int64_t p = gw; p < P.n_pairs; p += nw) {
         const uint8_t fl = P.flags[p];
         const unsigned long long key = P.keys_fwd[p];
@@ -74,28 +74,24 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
         if (lane == 0) {
             P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
             const int n2 = i + 1, m2 = j + 1;
-            const bool s16 = (fl & FLAG_S16) != 0;
-            const int rows = s16 ? P.rows_s16 : P.rows_s32;
+            const int route = flag_route(fl);
+            const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
             const uint32_t stripes = min((n2 + rows - 1) / rows, 0x3fff);
             P.nlen_rev[p] = n2;
             P.mlen_rev[p] = m2;
             P.target[p] = S;
             // reverse work items are grouped by S: the early-stopped sweep's length follows the
             // alignment's span, for which S is the available proxy
-            P.key_rev[p] = (s16 ? KEY_S16 : KEY_S32) | (stripes << 16) | (uint32_t)min(S, 0xffff);
+            P.key_rev[p] = route_key(route) | (stripes << 16) | (uint32_t)min(S, 0xffff);
             P.iota[p] = (int32_t)p;
-            if (s16) ++l16; else ++l32;
+            ++l_route[route];
         }
     }
-    if (lane == 0) {
-        if (l16) atomicAdd(&s_r16, l16);
-        if (l32) atomicAdd(&s_r32, l32);
-    }
+    if (lane == 0)
+        for (int r = 0; r < N_ROUTES; ++r)
+            if (l_route[r]) atomicAdd(&s_route[r], l_route[r]);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (s_r16) atomicAdd(&P.stats->n_rev_s16, s_r16);
-        if (s_r32) atomicAdd(&P.stats->n_rev_s32, s_r32);
-    }
+    if (threadIdx.x < N_ROUTES && s_route[threadIdx.x]) atomicAdd(&P.stats->rev_count[threadIdx.x], s_route[threadIdx.x]);
 }
 
 // After the reverse pass: q_start = q_end - i', r_start = r_end - j'.

@@ -9,15 +9,13 @@ namespace swb {
 // by the host once per batch to size grids and the stripe scratch.
 struct BatchStats {
     int32_t n_bad;          // invalid pairs
-    int32_t n_s16;          // valid, non-trivial pairs routed to the s16x2 path
-    int32_t n_s32;          // ... routed to the s32 path
     int32_t max_n;          // longest valid query
     int32_t max_m;          // longest valid reference
     int32_t malformed;      // offsets decrease somewhere -> whole batch invalid
-    int32_t n_rev_s16;      // pairs with S > 0 on each path (reverse pass)
-    int32_t n_rev_s32;
     int32_t internal_err;   // self-check failures (reverse max != forward S)
-    int32_t pad_;
+    int32_t pad_[3];
+    int32_t fwd_count[4];   // valid, non-trivial pairs per route (forward pass)
+    int32_t rev_count[4];   // pairs with S > 0 per route (reverse pass)
     unsigned long long cells;        // sum n*m over valid pairs
     unsigned long long swept_fwd;    // cells swept by the forward wavefront (incl. padding)
     unsigned long long swept_rev;    // cells swept by the reverse wavefront
@@ -33,6 +31,7 @@ struct PackParams {
     int64_t qshift, rshift;      // (payload + extent start) mod 16: code buffers keep the payload's alignment
     int alphabet;
     int s16_ok;                  // scoring fits the s16x2 path (int8 profile, int16 range)
+    int tag_ok;                  // the ROUTE_TAG kernel geometry supports row tags
     int max_sigma;
     int rows_s16, rows_s32;      // rows per stripe of each path
     uint8_t* qcode;              // [qN - q0]
@@ -120,17 +119,21 @@ __device__ __forceinline__ bool convert_run(const uint8_t* __restrict__ src, uin
 }
 
 __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
-    __shared__ int s_bad, s_s16, s_s32, s_maxn, s_maxm, s_malformed;
+    __shared__ int s_bad, s_route[N_ROUTES], s_maxn, s_maxm, s_malformed;
     __shared__ unsigned long long s_cells;
     __shared__ uint8_t lut[256];
-    if (threadIdx.x == 0) { s_bad = s_s16 = s_s32 = s_maxn = s_maxm = s_malformed = 0; s_cells = 0; }
+    if (threadIdx.x == 0) {
+        s_bad = s_maxn = s_maxm = s_malformed = 0;
+        for (int r = 0; r < N_ROUTES; ++r) s_route[r] = 0;
+        s_cells = 0;
+    }
     for (int c = threadIdx.x; c < 256; c += blockDim.x) lut[c] = ascii_code(P.alphabet, c);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint8_t pad_code = (uint8_t)((P.alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN) - 1);
-    int l_bad = 0, l_s16 = 0, l_s32 = 0, l_maxn = 0, l_maxm = 0, l_malf = 0;
+    int l_bad = 0, l_route[N_ROUTES] = {0, 0, 0}, l_maxn = 0, l_maxm = 0, l_malf = 0;
     unsigned long long l_cells = 0;
     for (int64_t p = gw; p < P.n_pairs; p += nw) {
         const int64_t qa = P.q_off[p], qb = P.q_off[p + 1];
@@ -161,13 +164,16 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
                 ++l_bad;
             } else {
                 nn = (int)n; mm = (int)m;
-                const bool s16 = P.s16_ok && (int64_t)P.max_sigma * (int64_t)min(nn, mm) <= 32000;
-                fl = s16 ? FLAG_S16 : 0;
+                // largest score the pair can reach (reading R13): picks the lane width
+                const int64_t smax = (int64_t)P.max_sigma * (int64_t)min(nn, mm);
+                const int route = (P.s16_ok && P.tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
+                                : (P.s16_ok && smax <= 32000) ? ROUTE_S16 : ROUTE_S32;
+                fl = route_flag(route);
                 if (nn > 0 && mm > 0) {
-                    const int rows = s16 ? P.rows_s16 : P.rows_s32;
+                    const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
                     const uint32_t stripes = min((nn + rows - 1) / rows, 0x3fff);
-                    key = (s16 ? KEY_S16 : KEY_S32) | (stripes << 16) | (uint32_t)mm;
-                    if (s16) ++l_s16; else ++l_s32;
+                    key = route_key(route) | (stripes << 16) | (uint32_t)mm;
+                    ++l_route[route];
                     l_cells += (unsigned long long)nn * (unsigned long long)mm;
                 }
                 l_maxn = max(l_maxn, nn);
@@ -184,8 +190,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
     }
     if (lane == 0) {
         if (l_bad) atomicAdd(&s_bad, l_bad);
-        if (l_s16) atomicAdd(&s_s16, l_s16);
-        if (l_s32) atomicAdd(&s_s32, l_s32);
+        for (int r = 0; r < N_ROUTES; ++r)
+            if (l_route[r]) atomicAdd(&s_route[r], l_route[r]);
         if (l_maxn) atomicMax(&s_maxn, l_maxn);
         if (l_maxm) atomicMax(&s_maxm, l_maxm);
         if (l_malf) atomicOr(&s_malformed, 1);
@@ -194,8 +200,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_bad) atomicAdd(&P.stats->n_bad, s_bad);
-        if (s_s16) atomicAdd(&P.stats->n_s16, s_s16);
-        if (s_s32) atomicAdd(&P.stats->n_s32, s_s32);
+        for (int r = 0; r < N_ROUTES; ++r)
+            if (s_route[r]) atomicAdd(&P.stats->fwd_count[r], s_route[r]);
         if (s_maxn) atomicMax(&P.stats->max_n, s_maxn);
         if (s_maxm) atomicMax(&P.stats->max_m, s_maxm);
         if (s_malformed) atomicOr(&P.stats->malformed, 1);

@@ -39,6 +39,25 @@
 #include "sw_common.cuh"
 #include "sw_pack.cuh"
 
+#ifndef SW_CELL_V2
+#define SW_CELL_V2 0
+#endif
+#ifndef SW_CELL_V3
+#define SW_CELL_V3 0
+#endif
+#ifndef SW_MIN_BLOCKS
+#define SW_MIN_BLOCKS 4
+#endif
+#ifndef SW_UNROLL
+#define SW_UNROLL 4
+#endif
+#ifndef SW_ABLATE
+#define SW_ABLATE 0        // timing experiments only (1: no improvement path, 2: no PRMT)
+#endif
+#ifndef SW_SINGLE_ONLY
+#define SW_SINGLE_ONLY 0   // experiment: compile only the single-stripe sweep
+#endif
+
 namespace swb {
 
 struct WaveParams {
@@ -48,15 +67,16 @@ struct WaveParams {
     const int64_t* rpos;        // reference code position per pair
     const int32_t* nlen;        // rows of each pair (forward: n, reverse: q_end+1)
     const int32_t* mlen;        // columns (forward: m, reverse: r_end+1)
-    const int32_t* order;       // pair ids sorted by work key
-    const int32_t* count;       // device: pairs on this path
-    const int32_t* first;       // device: index of this path's first pair in order (nullptr = 0)
+    const int32_t* order;       // pair ids sorted by work key (routes in order TAG, S16, S32)
+    const int32_t* counts;      // device: pairs per route for this pass
+    int route;                  // this launch's route
     const int32_t* target;      // reverse: forward score per pair
     unsigned long long* keys;   // per-pair atomicMax output
     int32_t* item_counter;      // work queue head (zeroed before launch)
     uint8_t* scratch;           // stripe hand-off rows
     int64_t scratch_seg_bytes;  // bytes of one segment x parity buffer
     unsigned long long* swept;  // cells swept (statistics)
+    uint32_t tag_mul;           // = 64; a kernel parameter so the row tag is an IMAD (FMA pipe), not a LEA
     Scoring sc;
 };
 
@@ -75,11 +95,19 @@ struct Geometry {
     static __host__ __device__ int warp_smem(int nc) { return prof_bytes(nc) + STOP_BYTES + 32 * T::NH * SVB; }
 };
 
-template <class T, int K>
-struct LaneState {
-    uint32_t HO[K];   // H + o of the lane's rows at the previous column
-    uint32_t E[K];    // E of the lane's rows at the previous column
-    uint32_t SV[K];   // HO of the column where the lane's best last improved
+// K 32-bit values kept as uint4 quads (so the improvement-column save can be
+// vector stores straight from the registers).
+template <int K>
+struct Quads {
+    uint4 q[(K + 3) / 4];
+    __device__ __forceinline__ uint32_t& operator[](int r) {
+        switch (r & 3) {
+            case 0: return q[r >> 2].x;
+            case 1: return q[r >> 2].y;
+            case 2: return q[r >> 2].z;
+            default: return q[r >> 2].w;
+        }
+    }
 };
 // Opaque copy of a value (keeps ptxas from turning `x * flag + b` back into a
 // SEL on the ALU pipe: the multiply-add then issues on the FMA pipe).
@@ -109,15 +137,17 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
 // read time).  Predicated STS.128 instead of per-row LOP3 merges keeps this
 // off the ALU pipe.
 template <int K>
-__device__ __forceinline__ void sv_store(uint32_t addr, const uint32_t (&HO)[K]) {
+__device__ __forceinline__ void sv_store(uint32_t addr, const Quads<K>& HO) {
 #pragma unroll
-    for (int w = 0; w < (K + 3) / 4; ++w) {
-        const uint32_t a = HO[4 * w];
-        const uint32_t b = (4 * w + 1 < K) ? HO[4 * w + 1] : 0u;
-        const uint32_t c = (4 * w + 2 < K) ? HO[4 * w + 2] : 0u;
-        const uint32_t d = (4 * w + 3 < K) ? HO[4 * w + 3] : 0u;
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr + 16 * w), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-    }
+    for (int w = 0; w < K / 4; ++w)
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr + 16 * w), "r"(HO.q[w].x), "r"(HO.q[w].y),
+                     "r"(HO.q[w].z), "r"(HO.q[w].w) : "memory");
+    if (K % 4 >= 2)
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(addr + 16 * (K / 4)), "r"(HO.q[K / 4].x),
+                     "r"(HO.q[K / 4].y) : "memory");
+    if (K % 4 == 1 || K % 4 == 3)
+        asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr + 16 * (K / 4) + 4 * (K % 4 - 1)),
+                     "r"(K % 4 == 1 ? HO.q[K / 4].x : HO.q[K / 4].z) : "memory");
 }
 
 // First row r of the saved column whose half h equals `target` (an HO value).
@@ -147,7 +177,7 @@ __device__ __forceinline__ unsigned long long pack_key(int S, int j, int i) {
 // every half emits after the sweep, which is exact when the item's
 // references differ by at most the pad margin (the columns past a shorter
 // reference are pad codes, whose cells stay below S).
-template <class T, int W, int K, bool REV, bool MULTI, bool EV>
+template <class T, int W, int K, bool REV, bool MULTI, bool EV, bool TAG>
 __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const uint32_t sv_base,
                                       const int seg, const int L, const int s_m, const int (&h_pid)[T::NH],
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
@@ -156,14 +186,23 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
-    constexpr int U = 4;                 // column unroll
+    constexpr int U = SW_UNROLL;         // column unroll (codes prefetched one block ahead)
     constexpr int CS = W * G::PB;        // profile bytes per code
     const int nc = P.sc.nc;
 
-    uint32_t HO[K], E[K];
+    Quads<K> HO;   // H + o of the lane's rows at the previous column
+    uint32_t E[K]; // E of the lane's rows at the previous column
 #pragma unroll
     for (int r = 0; r < K; ++r) { HO[r] = o2; E[r] = o2; }
-    uint32_t best = 0;
+    // TAG: the running max holds H*64 + (3 - u)*16 + (15 - r) for the cell of row r in the
+    // u-th column of the current 4-column block, so the max itself names the first column of
+    // the block and the smallest row holding it (reading R5).  Bookkeeping happens once per
+    // block; afterwards the 6 tag bits are set to ones so a later column with the same H never
+    // counts as an improvement.  Valid while H <= 511 (route eligibility).
+    static_assert(!TAG || (U <= 4 && K <= 16 && NH == 2), "TAG route geometry");
+    constexpr uint32_t TAGSET = 0x003f003fu;
+    uint32_t best = TAG ? TAGSET : 0u;
+    int brow[NH];                        // TAG: row of the half's last improvement
     int bc[NH];                          // column of the last strict improvement, per half
     uint32_t sv[NH];                     // shared address of the half's saved column
     int ev[NH];
@@ -171,6 +210,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
         bc[h] = 0;
+        brow[h] = 0;
         sv[h] = sv_base + (uint32_t)h * G::SVB;
         ev[h] = (EV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
         next_ev = min(next_ev, ev[h]);
@@ -189,11 +229,28 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     const uint32_t b0 = (L == 0) ? o2 : 0u;
 
     auto emit = [&](int h) {  // forward result of half h for this lane and stripe
-        const int b = T::get(best, h);
+        const int b = TAG ? (T::get(best, h) >> 6) : T::get(best, h);
         if (h_pid[h] >= 0 && b > 0) {
-            const int rr = sv_first_row<T, K>(sv[h], h, b + o);
+            const int rr = TAG ? brow[h] : sv_first_row<T, K>(sv[h], h, b + o);
             atomicMax(P.keys + h_pid[h], pack_key(b, bc[h], row0 + L * K + rr));
         }
+    };
+    // TAG: fold the block's running max into the per-half records (block start column t0)
+    auto tag_commit = [&](uint32_t nbt, int t0) {
+        const uint32_t d = nbt ^ best;
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            if ((d >> (16 * h)) & 0xffffu) {
+                const int v = T::get(nbt, h);
+                bc[h] = t0 + (U - 1 - ((v >> 4) & 3)) - L;
+                brow[h] = 15 - (v & 15);
+                if (REV && h_pid[h] >= 0 && (v >> 6) == h_tgt[h]) {
+                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], bc[h], row0 + L * K + brow[h]));
+                    atomicMin((int*)stop + seg * NH + h, bc[h] + W);
+                }
+            }
+        }
+        best = nbt | TAGSET;
     };
 
     // rotating prefetch of the next U columns' codes (and boundary rows)
@@ -214,6 +271,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
         T_end = te;
     }
     for (int t0 = 0; t0 < T_end; t0 += U) {
+        uint32_t nbt = best;  // TAG: running max of this block
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = t0 + u;
@@ -247,7 +305,9 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
 #pragma unroll
             for (int r = 0; r < K; ++r) {
                 uint32_t sc;
-                if (NH == 2) {
+                if (NH == 2 && (SW_ABLATE & 2)) {
+                    sc = pw[r & 1][r >> 2];  // timing ablation only: wrong scores
+                } else if (NH == 2) {
                     constexpr uint32_t SEL[4] = {0xC480u, 0xD591u, 0xE6A2u, 0xF7B3u};
                     sc = prmt(pw[0][r >> 2], pw[NH - 1][r >> 2], SEL[r & 3]);
                 } else {
@@ -255,42 +315,63 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 }
                 E[r] = T::addmax(E[r], e2, HO[r]);          // E[i][j] = max(E[i][j-1] + e, H[i][j-1] + o)
                 F = T::addmax(F, e2, hu);                   // F[i][j] = max(F[i-1][j] + e, H[i-1][j] + o)
+#if SW_CELL_V3
+                // the serial chain per row is F -> H -> HO; X = max(H[i-1][j-1] + s, E, 0)
+                // depends only on the previous column and can issue while the shuffle is in flight
+                const uint32_t x = T::addmax_relu(hd, sc, E[r]);
+                const uint32_t h = T::max2(x, F);            // F may be negative, x >= 0
+#elif SW_CELL_V2
+                // 3-op dependency chain per row (F -> H -> HO): the diagonal term is off the chain
+                const uint32_t x = T::add(hd, sc);          // H[i-1][j-1] + s
+                const uint32_t h = T::max3(x, E[r], F);     // max(., E, F, 0)
+#else
                 const uint32_t tt = T::max_relu(E[r], F);   // max(E, F, 0)
                 const uint32_t h = T::addmax(hd, sc, tt);   // max(H[i-1][j-1] + s, E, F, 0)
+#endif
                 hd = HO[r];
                 HO[r] = T::add(h, o2);
                 hu = HO[r];
-                H[r] = h;
+                // TAG: H*64 + tag per half, one IMAD on the FMA pipe (H <= 511: no carry)
+                H[r] = TAG ? h * P.tag_mul + (uint32_t)((U - 1 - u) * 16 + 15 - r) * 0x10001u : h;
             }
             hoLast = HO[K - 1];
             fLast = F;
             // running max over the lane's rows; strict improvement -> remember column + HO values
-            uint32_t nb = best;
+            if (TAG) {
 #pragma unroll
-            for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
-            if (K & 1) nb = T::max2(nb, H[K - 1]);
-            if (nb != best) {
-                const uint32_t d = nb ^ best;
+                for (int r = 0; r + 1 < K; r += 2) nbt = T::max3(nbt, H[r], H[r + 1]);
+                if (K & 1) nbt = T::max2(nbt, H[K - 1]);
+            } else {
+                uint32_t nb = best;
 #pragma unroll
-                for (int h = 0; h < NH; ++h) {
-                    if (NH == 1 || ((d >> (16 * h)) & 0xffffu)) {
-                        bc[h] = t - L;
-                        if (REV) {
-                            if (h_pid[h] >= 0 && T::get(nb, h) == h_tgt[h]) {
-                                int rr = 0;
+                for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
+                if (K & 1) nb = T::max2(nb, H[K - 1]);
+                if ((SW_ABLATE & 1) && !REV) {
+                    best = nb;  // timing ablation only: no improvement bookkeeping
+                } else if (nb != best) {
+                    const uint32_t d = nb ^ best;
 #pragma unroll
-                                for (int r = K - 1; r >= 0; --r) if (T::get(HO[r], h) == h_tgt[h] + o) rr = r;
-                                atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
-                                atomicMin((int*)stop + seg * NH + h, t - L + W);
+                    for (int h = 0; h < NH; ++h) {
+                        if (NH == 1 || ((d >> (16 * h)) & 0xffffu)) {
+                            bc[h] = t - L;
+                            if (REV) {
+                                if (h_pid[h] >= 0 && T::get(nb, h) == h_tgt[h]) {
+                                    int rr = 0;
+#pragma unroll
+                                    for (int r = K - 1; r >= 0; --r) if (T::get(HO[r], h) == h_tgt[h] + o) rr = r;
+                                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
+                                    atomicMin((int*)stop + seg * NH + h, t - L + W);
+                                }
+                            } else {
+                                sv_store<K>(sv[h], HO);
                             }
-                        } else {
-                            sv_store<K>(sv[h], HO);
                         }
                     }
+                    best = nb;
                 }
-                best = nb;
             }
             if (EV && t == next_ev) {
+                if (TAG) tag_commit(nbt, t0);  // make best / bc / brow current before emitting
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     if (ev[h] == t) {
@@ -299,6 +380,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                         ev[h] = 0x7fffffff;
                     }
                 }
+                if (TAG) nbt = best;
                 next_ev = ev[0];
                 if (NH == 2) next_ev = min(next_ev, ev[NH - 1]);
             }
@@ -307,6 +389,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
             }
         }
+        if (TAG && nbt != best) tag_commit(nbt, t0);
         if (REV) {
             __syncwarp();
             int te = 0;
@@ -321,11 +404,15 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     }
 }
 
-template <class T, int W, int K, bool REV>
-__global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
+template <class T, int W, int K, bool REV, bool TAG>
+__global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const WaveParams P) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
+    // Row/column tags are used only in forward sweeps without end events: there every
+    // computed cell past a reference is a pad cell (H < S <= 511), so H*64 cannot carry
+    // into the other half.  Event items and the reverse pass use the plain s16 logic.
+    constexpr bool TAGF = TAG && !REV;
     extern __shared__ __align__(16) uint8_t smem[];
 
     const int lane = threadIdx.x & 31;
@@ -339,8 +426,9 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
                              (uint32_t)(lane * NH * G::SVB);
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
-    const int n_path = *P.count;
-    const int first = P.first ? *P.first : 0;
+    const int n_path = P.counts[P.route];
+    int first = 0;
+    for (int r = 0; r < P.route; ++r) first += P.counts[r];
     const int items = (n_path + SLOTS - 1) / SLOTS;
     const uint32_t o2 = T::splat(P.sc.gap_open);
     const uint32_t e2 = T::splat(P.sc.gap_extend);
@@ -445,12 +533,12 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
             __syncwarp();
 
             // ---- the stripe's column sweep (single-stripe items skip all hand-off code) ----
-            if (ns == 1) {
+            if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
-                    sweep<T, W, K, REV, false, true>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    sweep<T, W, K, REV, false, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
                 else
-                    sweep<T, W, K, REV, false, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    sweep<T, W, K, REV, false, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                       row0, o2, e2, o, nullptr, nullptr, false, false);
             } else {
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
@@ -458,10 +546,10 @@ __global__ void __launch_bounds__(128) wavefront_kernel(const WaveParams P) {
                 uint2* scr_out = reinterpret_cast<uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
                 if (need_ev)
-                    sweep<T, W, K, REV, true, true>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    sweep<T, W, K, REV, true, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
                 else
-                    sweep<T, W, K, REV, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    sweep<T, W, K, REV, true, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
             }
         }

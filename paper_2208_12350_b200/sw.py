@@ -63,7 +63,8 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
+    # SW_B200_LIB: an alternative build of the same library (kernel-variant experiments)
+    path = os.environ.get("SW_B200_LIB", _build.LIB)
     if not os.path.exists(path):
         if not build_if_missing:
             raise OSError(f"{path} not built (run __graft_entry__.build())")
