@@ -23,7 +23,13 @@ namespace {
 
 // Kernel geometry of this build: 16-lane segments, 10 rows
 // per lane -> 160-row stripes (one stripe covers the ADEPT-shaped 150 bp reads).
-constexpr int W16 = 16, K16 = 10;
+#ifndef SW_W16
+#define SW_W16 16
+#endif
+#ifndef SW_K16
+#define SW_K16 10
+#endif
+constexpr int W16 = SW_W16, K16 = SW_K16;
 constexpr int W32 = 16, K32 = 10;
 constexpr int WARPS_PER_BLOCK = 4;
 constexpr int THREADS = WARPS_PER_BLOCK * 32;

@@ -48,6 +48,9 @@
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4
 #endif
+#ifndef SW_CODE_DIST
+#define SW_CODE_DIST 4     // reference-code prefetch distance in columns
+#endif
 #ifndef SW_UNROLL
 #define SW_UNROLL 4
 #endif
@@ -186,7 +189,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
-    constexpr int U = SW_UNROLL;         // column unroll (codes prefetched one block ahead)
+    constexpr int U = TAG ? (K <= 16 ? 4 : 2) : SW_UNROLL;  // column unroll (codes prefetched one block ahead)
     constexpr int CS = W * G::PB;        // profile bytes per code
     const int nc = P.sc.nc;
 
@@ -199,7 +202,10 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     // the block and the smallest row holding it (reading R5).  Bookkeeping happens once per
     // block; afterwards the 6 tag bits are set to ones so a later column with the same H never
     // counts as an improvement.  Valid while H <= 511 (route eligibility).
-    static_assert(!TAG || (U <= 4 && K <= 16 && NH == 2), "TAG route geometry");
+    // 6 tag bits: RB for the row (K <= 2^RB), the rest for the column within the block
+    constexpr int RB = K <= 16 ? 4 : 5;
+    constexpr int UB = 6 - RB;
+    static_assert(!TAG || ((U <= (1 << UB)) && K <= (1 << RB) && NH == 2), "TAG route geometry");
     constexpr uint32_t TAGSET = 0x003f003fu;
     uint32_t best = TAG ? TAGSET : 0u;
     int brow[NH];                        // TAG: row of the half's last improvement
@@ -242,8 +248,8 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
         for (int h = 0; h < NH; ++h) {
             if ((d >> (16 * h)) & 0xffffu) {
                 const int v = T::get(nbt, h);
-                bc[h] = t0 + (U - 1 - ((v >> 4) & 3)) - L;
-                brow[h] = 15 - (v & 15);
+                bc[h] = t0 + (U - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
+                brow[h] = ((1 << RB) - 1) - (v & ((1 << RB) - 1));
                 if (REV && h_pid[h] >= 0 && (v >> 6) == h_tgt[h]) {
                     atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], bc[h], row0 + L * K + brow[h]));
                     atomicMin((int*)stop + seg * NH + h, bc[h] + W);
@@ -254,12 +260,14 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     };
 
     // rotating prefetch of the next U columns' codes (and boundary rows)
-    uint32_t cd[U][NH];
+    constexpr int CD = SW_CODE_DIST < U ? SW_CODE_DIST : U;  // code prefetch distance (columns)
+    uint32_t cd[CD][NH];
     uint2 bnd[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
-        for (int h = 0; h < NH; ++h) cd[u][h] = ld_code(rp[h] + u);
+        for (int h = 0; h < NH; ++h)
+            if (u < CD) cd[u][h] = ld_code(rp[h] + u);
         if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
     }
 
@@ -279,14 +287,14 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
             uint32_t pw[NH][G::PWORDS];
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
-                const uint32_t src = prof_h[h] + cd[u][h] * cs;
+                const uint32_t src = prof_h[h] + cd[u % CD][h] * cs;
 #pragma unroll
                 for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
                     const uint4 v = lds128(src + 16 * q4);
                     pw[h][q4 * 4 + 0] = v.x; pw[h][q4 * 4 + 1] = v.y;
                     pw[h][q4 * 4 + 2] = v.z; pw[h][q4 * 4 + 3] = v.w;
                 }
-                cd[u][h] = ld_code(rp[h] + t + U);
+                cd[u % CD][h] = ld_code(rp[h] + t + CD);
             }
             uint32_t bHO = b0, bF = b0;
             if (MULTI) {
@@ -332,7 +340,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 HO[r] = T::add(h, o2);
                 hu = HO[r];
                 // TAG: H*64 + tag per half, one IMAD on the FMA pipe (H <= 511: no carry)
-                H[r] = TAG ? h * P.tag_mul + (uint32_t)((U - 1 - u) * 16 + 15 - r) * 0x10001u : h;
+                H[r] = TAG ? h * P.tag_mul + (uint32_t)((U - 1 - u) * (1 << RB) + (1 << RB) - 1 - r) * 0x10001u : h;
             }
             hoLast = HO[K - 1];
             fLast = F;
