@@ -355,6 +355,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     F.qcode = h->qcode.p; F.qrev = h->qrev.p; F.rcode = h->rcode.p; F.rrev = h->rrev.p;
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
     F.target = h->target.p; F.key_rev = h->key.p; F.iota = h->iota.p; F.rows_s16 = rows16; F.rows_s32 = rows32;
+    F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend;
     F.out = *out; F.stats = h->d_stats;
     {
         const int64_t warps = std::min<int64_t>(n_pairs, (int64_t)h->sm_count * 64);

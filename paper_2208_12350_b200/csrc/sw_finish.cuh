@@ -24,6 +24,7 @@ struct FinishParams {
     uint32_t* key_rev;
     int32_t* iota;
     int rows_s16, rows_s32;
+    int max_sigma, gap_extend;
     sw_result_t out;
     BatchStats* stats;
 };
@@ -73,7 +74,16 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
         for (int k = lane; k <= j; k += 32) P.rrev[rp + k] = P.rcode[rp + j - k];
         if (lane == 0) {
             P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
-            const int n2 = i + 1, m2 = j + 1;
+            const int n2 = i + 1;
+            // Columns the reverse pass can need (reading R6): every score-S alignment in the
+            // reversed rectangle starts at its origin (SURVEY.md 8(c) C-5 proof) and spans
+            // M + I columns, M <= n2 aligned pairs and I gap columns each costing >= |e|, so
+            // S <= max_s*M - |e|*I  =>  columns <= n2 + (max_s*n2 - S) / |e|.  Exact bound.
+            int m2 = j + 1;
+            if (P.gap_extend < 0) {
+                const long long bound = (long long)n2 + ((long long)P.max_sigma * n2 - S) / (long long)(-P.gap_extend);
+                if (bound < m2) m2 = (int)max(bound, 1LL);
+            }
             const int route = flag_route(fl);
             const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
             const uint32_t stripes = min((n2 + rows - 1) / rows, 0x3fff);
