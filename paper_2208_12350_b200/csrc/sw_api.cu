@@ -30,10 +30,13 @@ namespace {
 #define SW_K16 10
 #endif
 constexpr int W16 = SW_W16, K16 = SW_K16;
+// protein: 8 rows per lane keep the 25-code int8 profile at 8 bytes per (code, lane) -> 12.8 KB per
+// warp, so shared memory allows 16 resident warps per SM (10 rows would need 16-byte entries)
+constexpr int WP = 16, KP = 8;
 constexpr int W32 = 16, K32 = 10;
 constexpr int WARPS_PER_BLOCK = 4;
-constexpr int THREADS = WARPS_PER_BLOCK * 32;
 using G16 = Geometry<W16, K16, TS16>;
+using GP = Geometry<WP, KP, TS16>;
 using G32 = Geometry<W32, K32, TS32>;
 
 template <class T>
@@ -163,24 +166,26 @@ void set_smem_attr(K kernel, int bytes) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-int occupancy_blocks(const void* kernel, int smem) {
+int occupancy_blocks(const void* kernel, int threads, int smem) {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, THREADS, smem) != cudaSuccess) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess) nb = 1;
     return std::max(nb, 1);
 }
 
 struct Launch {
     int blocks = 0;
     int smem = 0;
+    int warps = WARPS_PER_BLOCK;  // warps per block
 };
 
 template <class G>
-Launch plan_wave(const sw_context* h, const void* kernel, int nc, int64_t n_path) {
+Launch plan_wave(const sw_context* h, const void* kernel, int nc, int64_t n_path, int warps = WARPS_PER_BLOCK) {
     Launch l;
-    l.smem = WARPS_PER_BLOCK * G::warp_smem(nc);
+    l.warps = warps;
+    l.smem = warps * G::warp_smem(nc);
     const int64_t items = (n_path + G::SLOTS - 1) / G::SLOTS;
-    const int64_t need = (items + WARPS_PER_BLOCK - 1) / WARPS_PER_BLOCK;
-    const int64_t maxb = (int64_t)h->sm_count * occupancy_blocks(kernel, l.smem);
+    const int64_t need = (items + warps - 1) / warps;
+    const int64_t maxb = (int64_t)h->sm_count * occupancy_blocks(kernel, warps * 32, l.smem);
     l.blocks = (int)std::max<int64_t>(0, std::min(need, maxb));
     return l;
 }
@@ -256,7 +261,8 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         ENS(cub_temp, tb);
     }
 
-    const int rows16 = G16::ROWS, rows32 = G32::ROWS;
+    const bool protein = sc.alphabet == SW_ALPHABET_PROTEIN;
+    const int rows16 = protein ? GP::ROWS : G16::ROWS, rows32 = G32::ROWS;
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[0], s));
 
     // 3. pack
@@ -288,11 +294,15 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[2], s));
 
     // one kernel per route and pass (routes: TAG, S16, S32; sw_common.cuh)
-    const void* kfwd[N_ROUTES] = {(const void*)wavefront_kernel<TS16, W16, K16, false, true>,
-                                  (const void*)wavefront_kernel<TS16, W16, K16, false, false>,
+    const void* kfwd[N_ROUTES] = {protein ? (const void*)wavefront_kernel<TS16, WP, KP, false, true>
+                                          : (const void*)wavefront_kernel<TS16, W16, K16, false, true>,
+                                  protein ? (const void*)wavefront_kernel<TS16, WP, KP, false, false>
+                                          : (const void*)wavefront_kernel<TS16, W16, K16, false, false>,
                                   (const void*)wavefront_kernel<TS32, W32, K32, false, false>};
-    const void* krev[N_ROUTES] = {(const void*)wavefront_kernel<TS16, W16, K16, true, true>,
-                                  (const void*)wavefront_kernel<TS16, W16, K16, true, false>,
+    const void* krev[N_ROUTES] = {protein ? (const void*)wavefront_kernel<TS16, WP, KP, true, true>
+                                          : (const void*)wavefront_kernel<TS16, W16, K16, true, true>,
+                                  protein ? (const void*)wavefront_kernel<TS16, WP, KP, true, false>
+                                          : (const void*)wavefront_kernel<TS16, W16, K16, true, false>,
                                   (const void*)wavefront_kernel<TS32, W32, K32, true, false>};
     Launch lf[N_ROUTES], lr[N_ROUTES];
     for (int r = 0; r < N_ROUTES; ++r) {
@@ -300,6 +310,10 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         if (r == ROUTE_S32) {
             lf[r] = plan_wave<G32>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
             lr[r] = plan_wave<G32>(h, krev[r], sc.nc, hs.fwd_count[r]);
+        } else if (protein) {
+            // 3-warp blocks: 5 blocks x 3 warps fit the SM's shared memory (4-warp blocks: only 3)
+            lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], 3);
+            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, hs.fwd_count[r], 3);
         } else {
             lf[r] = plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
             lr[r] = plan_wave<G16>(h, krev[r], sc.nc, hs.fwd_count[r]);
@@ -313,10 +327,10 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16) * 8;
         for (int r = 0; r < N_ROUTES; ++r) {
             const int rows = r == ROUTE_S32 ? rows32 : rows16;
-            const int segs = r == ROUTE_S32 ? G32::SEGS : G16::SEGS;
+            const int segs = r == ROUTE_S32 ? G32::SEGS : protein ? GP::SEGS : G16::SEGS;
             if (hs.fwd_count[r] && hs.max_n > rows) {
                 seg_bytes = row_bytes;
-                need = std::max(need, (size_t)std::max(lf[r].blocks, lr[r].blocks) * WARPS_PER_BLOCK * segs * 2 * row_bytes);
+                need = std::max(need, (size_t)std::max(lf[r].blocks * lf[r].warps, lr[r].blocks * lr[r].warps) * segs * 2 * row_bytes);
             }
         }
         if (need) ENS(scratch, need);
@@ -344,7 +358,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         W.route = r;
         W.item_counter = h->d_counters + r;
         void* args[] = {&W};
-        SW_CUDA(h, cudaLaunchKernel(kfwd[r], dim3(lf[r].blocks), dim3(THREADS), args, (size_t)lf[r].smem, s));
+        SW_CUDA(h, cudaLaunchKernel(kfwd[r], dim3(lf[r].blocks), dim3(lf[r].warps * 32), args, (size_t)lf[r].smem, s));
         ++h->own_launches;
     }
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[4], s));
@@ -380,7 +394,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         W.route = r;
         W.item_counter = h->d_counters + 4 + r;
         void* args[] = {&W};
-        SW_CUDA(h, cudaLaunchKernel(krev[r], dim3(lr[r].blocks), dim3(THREADS), args, (size_t)lr[r].smem, s));
+        SW_CUDA(h, cudaLaunchKernel(krev[r], dim3(lr[r].blocks), dim3(lr[r].warps * 32), args, (size_t)lr[r].smem, s));
         ++h->own_launches;
     }
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[6], s));
@@ -435,6 +449,10 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
     h->sm_count = p.multiProcessorCount;
     // opt in to large dynamic shared memory (protein profiles)
     const int big = 200 * 1024;
+    set_smem_attr(wavefront_kernel<TS16, WP, KP, false, true>, big);
+    set_smem_attr(wavefront_kernel<TS16, WP, KP, true, true>, big);
+    set_smem_attr(wavefront_kernel<TS16, WP, KP, false, false>, big);
+    set_smem_attr(wavefront_kernel<TS16, WP, KP, true, false>, big);
     set_smem_attr(wavefront_kernel<TS16, W16, K16, false, true>, big);
     set_smem_attr(wavefront_kernel<TS16, W16, K16, true, true>, big);
     set_smem_attr(wavefront_kernel<TS16, W16, K16, false, false>, big);

@@ -89,7 +89,8 @@ struct Geometry {
     static constexpr int SLOTS = SEGS * T::NH;
     static constexpr int ROWS = W * K;                       // rows per stripe
     // profile bytes per (slot, code, lane): int8 x K (s16x2) or int32 x K (s32), 16 B aligned
-    static constexpr int PB = (T::NH == 2) ? 16 * ((K + 15) / 16) : 16 * ((4 * K + 15) / 16);
+    // int8 profile: 4/8/16-byte entries (one LDS.32/.64/.128 per 4/8/16 rows); int32: 16-byte multiples
+    static constexpr int PB = (T::NH == 2) ? (K <= 4 ? 4 : K <= 8 ? 8 : 16 * ((K + 15) / 16)) : 16 * ((4 * K + 15) / 16);
     static constexpr int PWORDS = PB / 4;
     static constexpr int SVB = 16 * ((4 * K + 15) / 16);    // saved improvement column per (lane, half)
     static __host__ __device__ int prof_bytes(int nc) { return SLOTS * nc * W * PB; }
@@ -171,6 +172,14 @@ __device__ __forceinline__ int sv_first_row(uint32_t addr, int h, int target) {
 __device__ __forceinline__ unsigned long long pack_key(int S, int j, int i) {
     return ((unsigned long long)(uint32_t)S << 32) | ((unsigned long long)(0xffff - j) << 16) |
            (unsigned long long)(0xffff - i);
+}
+
+template <int R>
+__device__ __forceinline__ uint4 lds_rem(uint32_t addr) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (R == 1) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v.x) : "r"(addr));
+    if (R == 2) asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
 }
 
 // One stripe of one work item: the column sweep of the anti-diagonal
@@ -288,11 +297,17 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
                 const uint32_t src = prof_h[h] + cd[u % CD][h] * cs;
+                if (G::PWORDS >= 4) {
 #pragma unroll
-                for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
-                    const uint4 v = lds128(src + 16 * q4);
-                    pw[h][q4 * 4 + 0] = v.x; pw[h][q4 * 4 + 1] = v.y;
-                    pw[h][q4 * 4 + 2] = v.z; pw[h][q4 * 4 + 3] = v.w;
+                    for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
+                        const uint4 v = lds128(src + 16 * q4);
+                        pw[h][q4 * 4 + 0] = v.x; pw[h][q4 * 4 + 1] = v.y;
+                        pw[h][q4 * 4 + 2] = v.z; pw[h][q4 * 4 + 3] = v.w;
+                    }
+                } else {
+                    const uint4 v = lds_rem<G::PWORDS>(src);
+                    pw[h][0] = v.x;
+                    if (G::PWORDS > 1) pw[h][G::PWORDS - 1] = v.y;
                 }
                 cd[u % CD][h] = ld_code(rp[h] + t + CD);
             }
