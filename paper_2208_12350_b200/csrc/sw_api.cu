@@ -271,7 +271,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         PackParams P;
         P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.n_pairs = n_pairs;
         P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
-        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = K16 <= 16 ? 1 : 0;
+        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA) ? 1 : 0;  // TAG route: DNA batches
         P.rows_s16 = rows16; P.rows_s32 = rows32;
         P.qcode = h->qcode.p; P.rcode = h->rcode.p; P.rrev = h->rrev.p;
         P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;

@@ -437,6 +437,17 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
     // into the other half.  Event items and the reverse pass use the plain s16 logic.
     constexpr bool TAGF = TAG && !REV;
     extern __shared__ __align__(16) uint8_t smem[];
+    // substitution table for the profile builds, in shared memory: lanes index it with
+    // divergent codes, which a constant-bank table would serialise
+    __shared__ int8_t s_sigma[24 * 24];
+    for (int k = threadIdx.x; k < 24 * 24; k += blockDim.x) {
+        const int a = k / 24, b = k % 24;
+        s_sigma[k] = (int8_t)(P.sc.alphabet == SW_ALPHABET_DNA ? 0 : c_blosum62[a][b]);
+    }
+    __syncthreads();
+    auto sigma = [&](int a, int b) -> int {
+        return P.sc.alphabet == SW_ALPHABET_DNA ? (a == b ? P.sc.match : P.sc.mismatch) : (int)s_sigma[a * 24 + b];
+    };
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -536,7 +547,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
 #pragma unroll
                             for (int b = 0; b < 4; ++b) {
                                 int v = -128;
-                                if (qc[b] >= 0 && c < nc - 1) v = sigma_of(P.sc, qc[b], c) - o;
+                                if (qc[b] >= 0 && c < nc - 1) v = sigma(qc[b], c) - o;
                                 word |= (uint32_t)(v & 0xff) << (8 * b);
                             }
                             *reinterpret_cast<uint32_t*>(base + (size_t)c * W * G::PB) = word;
@@ -547,7 +558,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
                         const int qc = (pid >= 0 && r < K && i < n) ? P.qcode[qp + i] : -1;
                         for (int c = 0; c < nc; ++c) {
                             int v = -(1 << 29);
-                            if (qc >= 0 && c < nc - 1) v = sigma_of(P.sc, qc, c) - o;
+                            if (qc >= 0 && c < nc - 1) v = sigma(qc, c) - o;
                             *reinterpret_cast<int32_t*>(base + (size_t)c * W * G::PB) = v;
                         }
                     }
