@@ -150,7 +150,7 @@ __device__ __forceinline__ void sv_store(uint32_t addr, const Quads<K>& HO) {
         asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(addr + 16 * (K / 4)), "r"(HO.q[K / 4].x),
                      "r"(HO.q[K / 4].y) : "memory");
     if (K % 4 == 1 || K % 4 == 3)
-        asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr + 16 * (K / 4) + 4 * (K % 4 - 1)),
+        asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr + 16 * (K / 4) + (K % 4 == 3 ? 8u : 0u)),
                      "r"(K % 4 == 1 ? HO.q[K / 4].x : HO.q[K / 4].z) : "memory");
 }
 
@@ -280,6 +280,11 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
         if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
     }
 
+    // reverse pass: packed targets of both halves (the forward score S of each pair)
+    uint32_t tgt2 = 0;
+#pragma unroll
+    for (int h = 0; h < NH; ++h) tgt2 = T::set(tgt2, h, h_pid[h] >= 0 ? h_tgt[h] : -1);
+    int found_blk = 0;
     int T_end = mmax + W - 1;
     if (REV) {
         int te = 0;
@@ -365,11 +370,29 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 for (int r = 0; r + 1 < K; r += 2) nbt = T::max3(nbt, H[r], H[r + 1]);
                 if (K & 1) nbt = T::max2(nbt, H[K - 1]);
             } else {
-                uint32_t nb = best;
+                uint32_t nb = REV ? H[0] : best;
 #pragma unroll
-                for (int r = 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
-                if (K & 1) nb = T::max2(nb, H[K - 1]);
-                if ((SW_ABLATE & 1) && !REV) {
+                for (int r = REV ? 1 : 0; r + 1 < K; r += 2) nb = T::max3(nb, H[r], H[r + 1]);
+                if ((K & 1) != (REV ? 1 : 0)) nb = T::max2(nb, H[K - 1]);
+                if (REV) {
+                    // reverse pass: only cells equal to S matter (reading R6).  nb is this column's max;
+                    // a half whose target was found gets the unreachable target -1.
+                    const uint32_t x = nb ^ tgt2;
+                    if (NH == 1 ? x == 0u : (((x & 0xffffu) == 0u) || ((x >> 16) == 0u))) {
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) {
+                            if (((x >> (16 * h)) & (NH == 1 ? 0xffffffffu : 0xffffu)) == 0u && h_pid[h] >= 0) {
+                                int rr = 0;
+#pragma unroll
+                                for (int r = K - 1; r >= 0; --r) if (T::get(H[r], h) == h_tgt[h]) rr = r;
+                                atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
+                                atomicMin((int*)stop + seg * NH + h, t - L + W);
+                                tgt2 = T::set(tgt2, h, -1);
+                                found_blk = 1;
+                            }
+                        }
+                    }
+                } else if (SW_ABLATE & 1) {
                     best = nb;  // timing ablation only: no improvement bookkeeping
                 } else if (nb != best) {
                     const uint32_t d = nb ^ best;
@@ -377,17 +400,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                     for (int h = 0; h < NH; ++h) {
                         if (NH == 1 || ((d >> (16 * h)) & 0xffffu)) {
                             bc[h] = t - L;
-                            if (REV) {
-                                if (h_pid[h] >= 0 && T::get(nb, h) == h_tgt[h]) {
-                                    int rr = 0;
-#pragma unroll
-                                    for (int r = K - 1; r >= 0; --r) if (T::get(HO[r], h) == h_tgt[h] + o) rr = r;
-                                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
-                                    atomicMin((int*)stop + seg * NH + h, t - L + W);
-                                }
-                            } else {
-                                sv_store<K>(sv[h], HO);
-                            }
+                            sv_store<K>(sv[h], HO);
                         }
                     }
                     best = nb;
@@ -413,12 +426,13 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
             }
         }
         if (TAG && nbt != best) tag_commit(nbt, t0);
-        if (REV) {
+        if (REV && __any_sync(FULL, found_blk)) {  // re-read the stop columns only after a find
             __syncwarp();
             int te = 0;
 #pragma unroll
             for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_m, sl) + W - 1, stop[sl]));
             T_end = te;
+            found_blk = 0;
         }
     }
     if (!REV && !EV) {
