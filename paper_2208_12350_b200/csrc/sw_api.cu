@@ -47,6 +47,8 @@ struct DevBuf {
 
 }  // namespace
 
+constexpr int MAX_CHUNKS = 4;
+
 struct sw_context {
     int device = 0;
     int sm_count = 0;
@@ -77,6 +79,8 @@ struct sw_context {
     DevBuf<int32_t> st_out;
 
     int codes_alphabet = -1;  // alphabet the code buffers were last cleared for
+    cudaStream_t copy_stream = nullptr;  // host-buffer entry point: overlapped copies
+    cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
     bool timing = false;
     cudaEvent_t ev[8] = {};
     bool ev_valid = false;
@@ -190,10 +194,20 @@ Launch plan_wave(const sw_context* h, const void* kernel, int nc, int64_t n_path
     return l;
 }
 
+// What the host already knows about a batch (host-buffer entry point): with it the
+// pipeline needs no stream synchronisation between enqueueing and completion.
+struct HostPlan {
+    int64_t ext[4];            // q0, qN, r0, rN
+    int32_t max_n, max_m;      // longest query / reference of the batch
+    int32_t route_upper[N_ROUTES];  // pairs per route by lengths alone (>= the device's counts)
+    bool reset_cumulative;     // first chunk of a user call
+};
+
 // The batch pipeline on device pointers.  host_ext (optional) = {q0, qN, r0, rN}.
 sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_off, const uint8_t* refs,
                        const int64_t* r_off, int64_t n_pairs, const sw_scoring_t* scoring,
-                       const sw_result_t* out, cudaStream_t s, const int64_t* host_ext) {
+                       const sw_result_t* out, cudaStream_t s, const int64_t* host_ext,
+                       const HostPlan* hp = nullptr) {
     int dev = -1;
     SW_CUDA(h, cudaGetDevice(&dev));
     if (dev != h->device) return fail(h, SW_ERR_WRONG_DEVICE, "current device differs from the handle's device");
@@ -203,8 +217,10 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (st != SW_OK) return st;
     if (n_pairs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs < 0");
     if (n_pairs > 0x7ffffff0LL) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs exceeds 2^31 - 16");
-    h->own_launches = 0;
-    h->lib_launches = 0;
+    if (!hp || hp->reset_cumulative) {
+        h->own_launches = 0;
+        h->lib_launches = 0;
+    }
     h->ev_valid = false;
     if (n_pairs == 0) return SW_OK;
     if (!queries || !q_off || !refs || !r_off || !out || !out->score || !out->q_end || !out->r_end ||
@@ -215,7 +231,9 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
 
     // 1. payload extents
     int64_t ext[4];
-    if (host_ext) {
+    if (hp) {
+        std::memcpy(ext, hp->ext, sizeof(ext));
+    } else if (host_ext) {
         std::memcpy(ext, host_ext, sizeof(ext));
     } else {
         SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 0, q_off, 8, cudaMemcpyDeviceToHost, s));
@@ -266,7 +284,9 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[0], s));
 
     // 3. pack
-    SW_CUDA(h, cudaMemsetAsync(h->d_stats, 0, sizeof(BatchStats), s));
+    if (!hp || hp->reset_cumulative) SW_CUDA(h, cudaMemsetAsync(h->d_stats, 0, sizeof(BatchStats), s));
+    else SW_CUDA(h, cudaMemsetAsync(reinterpret_cast<uint8_t*>(h->d_stats) + STATS_PER_BATCH_OFFSET, 0,
+                                    sizeof(BatchStats) - STATS_PER_BATCH_OFFSET, s));
     {
         PackParams P;
         P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.n_pairs = n_pairs;
@@ -283,10 +303,18 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         ++h->own_launches;
     }
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
-    // 4. statistics -> grids and scratch
-    SW_CUDA(h, cudaMemcpyAsync(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
-    SW_CUDA(h, cudaStreamSynchronize(s));
-    const BatchStats hs = *h->h_stats;
+    // 4. statistics -> grids and scratch (read back, unless the host already knows bounds)
+    BatchStats hs;
+    if (hp) {
+        std::memset(&hs, 0, sizeof(hs));
+        hs.max_n = hp->max_n;
+        hs.max_m = hp->max_m;
+        for (int r = 0; r < N_ROUTES; ++r) hs.fwd_count[r] = hp->route_upper[r];
+    } else {
+        SW_CUDA(h, cudaMemcpyAsync(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
+        SW_CUDA(h, cudaStreamSynchronize(s));
+        hs = *h->h_stats;
+    }
     if (hs.malformed) {
         fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, n_pairs);
         return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
@@ -471,6 +499,11 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
     for (auto& ev : h->ev) {
         if (cudaEventCreate(&ev) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
     }
+    for (int k = 0; k < 8; ++k) {
+        if (cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
+    }
+    if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
     *handle = h;
     return SW_OK;
 }
@@ -490,30 +523,93 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
     if (n_pairs == 0) return SW_OK;
     if (!queries || !q_offsets || !refs || !r_offsets || !out_host)
         return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+    Scoring sc;
+    bool s16_ok = false;
+    sw_status_t st = check_scoring(h, scoring, sc, s16_ok);
+    if (st != SW_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    const int64_t ext[4] = {q_offsets[0], q_offsets[n_pairs], r_offsets[0], r_offsets[n_pairs]};
-    if (ext[1] < ext[0] || ext[3] < ext[2]) return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
     const size_t N = (size_t)n_pairs;
-    const size_t tq = (size_t)(ext[1] - ext[0]), tr = (size_t)(ext[3] - ext[2]);
+    int32_t* dst[5] = {out_host->score, out_host->q_end, out_host->r_end, out_host->q_start, out_host->r_start};
+    // host-side validation: offsets must be non-decreasing (reading R15)
+    for (int64_t p = 0; p < n_pairs; ++p) {
+        if (q_offsets[p + 1] < q_offsets[p] || r_offsets[p + 1] < r_offsets[p]) {
+            for (int k = 0; k < 5; ++k)
+                if (dst[k]) for (size_t i = 0; i < N; ++i) dst[k][i] = -1;
+            return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
+        }
+    }
+    const int64_t q0 = q_offsets[0], qN = q_offsets[n_pairs], r0 = r_offsets[0], rN = r_offsets[n_pairs];
+    const size_t tq = (size_t)(qN - q0), tr = (size_t)(rN - r0);
 #define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
     ENS(st_q, tq + 1); ENS(st_r, tr + 1); ENS(st_qo, N + 1); ENS(st_ro, N + 1); ENS(st_out, 5 * N);
 #undef ENS
-    // device copies keep the caller's offsets; payload pointer is shifted so offsets stay valid
-    SW_CUDA(h, cudaMemcpyAsync(h->st_q.p, queries + ext[0], tq, cudaMemcpyHostToDevice, s));
-    SW_CUDA(h, cudaMemcpyAsync(h->st_r.p, refs + ext[2], tr, cudaMemcpyHostToDevice, s));
-    SW_CUDA(h, cudaMemcpyAsync(h->st_qo.p, q_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, s));
-    SW_CUDA(h, cudaMemcpyAsync(h->st_ro.p, r_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, s));
-    sw_result_t dout;
-    dout.score = h->st_out.p; dout.q_end = h->st_out.p + N; dout.r_end = h->st_out.p + 2 * N;
-    dout.q_start = h->st_out.p + 3 * N; dout.r_start = h->st_out.p + 4 * N;
-    sw_status_t st = align_impl(h, h->st_q.p - ext[0], h->st_qo.p, h->st_r.p - ext[2], h->st_ro.p, n_pairs, scoring,
-                                &dout, s, ext);
-    if (st != SW_OK && st != SW_ERR_INVALID_ARGUMENT) return st;
-    int32_t* dst[5] = {out_host->score, out_host->q_end, out_host->r_end, out_host->q_start, out_host->r_start};
-    for (int k = 0; k < 5; ++k)
-        if (dst[k]) SW_CUDA(h, cudaMemcpyAsync(dst[k], h->st_out.p + k * N, N * 4, cudaMemcpyDeviceToHost, s));
+    // Chunks of about equal cell count; chunk k+1's host-to-device copy (copy stream) overlaps
+    // chunk k's kernels (caller's stream), and chunk k's results return while k+1 computes.
+    const bool protein = sc.alphabet == SW_ALPHABET_PROTEIN;
+    const int rows16 = protein ? GP::ROWS : G16::ROWS;
+    const bool tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA);
+    double total_cells = 0;
+    for (int64_t p = 0; p < n_pairs; ++p)
+        total_cells += (double)(q_offsets[p + 1] - q_offsets[p]) * (double)(r_offsets[p + 1] - r_offsets[p]);
+    const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(MAX_CHUNKS, n_pairs / 16384));
+    int64_t cut[MAX_CHUNKS + 1];
+    cut[0] = 0;
+    {
+        double acc = 0;
+        int k = 1;
+        for (int64_t p = 0; p < n_pairs && k < n_chunks; ++p) {
+            acc += (double)(q_offsets[p + 1] - q_offsets[p]) * (double)(r_offsets[p + 1] - r_offsets[p]);
+            if (acc >= total_cells * k / n_chunks) cut[k++] = p + 1;
+        }
+        while (k <= n_chunks) cut[k++] = n_pairs;
+    }
+    // all input copies first (offsets whole, payload per chunk)
+    SW_CUDA(h, cudaMemcpyAsync(h->st_qo.p, q_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, h->copy_stream));
+    SW_CUDA(h, cudaMemcpyAsync(h->st_ro.p, r_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, h->copy_stream));
+    for (int k = 0; k < n_chunks; ++k) {
+        const int64_t a = cut[k], b = cut[k + 1];
+        const int64_t qa = q_offsets[a], qb = q_offsets[b], ra = r_offsets[a], rb = r_offsets[b];
+        if (qb > qa) SW_CUDA(h, cudaMemcpyAsync(h->st_q.p + (qa - q0), queries + qa, (size_t)(qb - qa), cudaMemcpyHostToDevice, h->copy_stream));
+        if (rb > ra) SW_CUDA(h, cudaMemcpyAsync(h->st_r.p + (ra - r0), refs + ra, (size_t)(rb - ra), cudaMemcpyHostToDevice, h->copy_stream));
+        SW_CUDA(h, cudaEventRecord(h->ev_in[k], h->copy_stream));
+    }
+    sw_status_t result = SW_OK;
+    for (int k = 0; k < n_chunks; ++k) {
+        const int64_t a = cut[k], b = cut[k + 1];
+        if (b <= a) continue;
+        HostPlan hp;
+        hp.ext[0] = q_offsets[a]; hp.ext[1] = q_offsets[b]; hp.ext[2] = r_offsets[a]; hp.ext[3] = r_offsets[b];
+        hp.max_n = 0; hp.max_m = 0;
+        for (int r = 0; r < N_ROUTES; ++r) hp.route_upper[r] = 0;
+        for (int64_t p = a; p < b; ++p) {
+            const int64_t n = q_offsets[p + 1] - q_offsets[p], m = r_offsets[p + 1] - r_offsets[p];
+            if (n > SW_MAX_SEQ_LEN || m > SW_MAX_SEQ_LEN) continue;  // invalid pair
+            hp.max_n = std::max<int32_t>(hp.max_n, (int32_t)n);
+            hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
+            if (n == 0 || m == 0) continue;
+            const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
+            const int route = (s16_ok && tag_ok && smax <= TAG_MAX_SCORE && n <= rows16) ? ROUTE_TAG
+                            : (s16_ok && smax <= 32000) ? ROUTE_S16 : ROUTE_S32;
+            ++hp.route_upper[route];
+        }
+        hp.reset_cumulative = k == 0;
+        SW_CUDA(h, cudaStreamWaitEvent(s, h->ev_in[k], 0));
+        sw_result_t dout;
+        dout.score = h->st_out.p + a; dout.q_end = h->st_out.p + N + a; dout.r_end = h->st_out.p + 2 * N + a;
+        dout.q_start = h->st_out.p + 3 * N + a; dout.r_start = h->st_out.p + 4 * N + a;
+        st = align_impl(h, h->st_q.p - q0, h->st_qo.p + a, h->st_r.p - r0, h->st_ro.p + a, b - a, scoring, &dout, s,
+                        nullptr, &hp);  // launch counters accumulate over the chunks
+        if (st != SW_OK) { result = st; break; }
+        SW_CUDA(h, cudaEventRecord(h->ev_out[k], s));
+        SW_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_out[k], 0));
+        for (int f = 0; f < 5; ++f)
+            if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f] + a, h->st_out.p + f * N + a, (size_t)(b - a) * 4,
+                                                   cudaMemcpyDeviceToHost, h->copy_stream));
+    }
+    SW_CUDA(h, cudaStreamSynchronize(h->copy_stream));
     SW_CUDA(h, cudaStreamSynchronize(s));
-    return st;
+    h->last_stream = s;
+    return result;
 }
 
 sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs) {
@@ -546,6 +642,11 @@ sw_status_t sw_free(sw_handle_t h) {
     if (h->d_counters) cudaFree(h->d_counters);
     if (h->d_sink) cudaFree(h->d_sink);
     for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
+    for (int k = 0; k < 8; ++k) {
+        if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
+        if (h->ev_out[k]) cudaEventDestroy(h->ev_out[k]);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     delete h;
     return SW_OK;
 }

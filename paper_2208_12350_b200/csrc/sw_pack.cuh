@@ -1,6 +1,7 @@
 // sw_pack.cuh -- step a1 of SURVEY.md sec. 8(a): validation, ASCII -> codes,
 // per-pair lengths/flags/work keys and batch statistics, in one pass.
 #pragma once
+#include <cstddef>
 #include "sw_common.cuh"
 
 namespace swb {
@@ -8,18 +9,21 @@ namespace swb {
 // Batch statistics written by the pack / finish kernels (device), read back
 // by the host once per batch to size grids and the stripe scratch.
 struct BatchStats {
+    // cumulative over a user call (sw_align_batch_host may run several chunks)
     int32_t n_bad;          // invalid pairs
-    int32_t max_n;          // longest valid query
-    int32_t max_m;          // longest valid reference
-    int32_t malformed;      // offsets decrease somewhere -> whole batch invalid
     int32_t internal_err;   // self-check failures (reverse max != forward S)
-    int32_t pad_[3];
-    int32_t fwd_count[4];   // valid, non-trivial pairs per route (forward pass)
-    int32_t rev_count[4];   // pairs with S > 0 per route (reverse pass)
     unsigned long long cells;        // sum n*m over valid pairs
     unsigned long long swept_fwd;    // cells swept by the forward wavefront (incl. padding)
     unsigned long long swept_rev;    // cells swept by the reverse wavefront
+    // per batch (chunk)
+    int32_t max_n;          // longest valid query
+    int32_t max_m;          // longest valid reference
+    int32_t malformed;      // offsets decrease somewhere -> whole batch invalid
+    int32_t pad_;
+    int32_t fwd_count[4];   // valid, non-trivial pairs per route (forward pass)
+    int32_t rev_count[4];   // pairs with S > 0 per route (reverse pass)
 };
+constexpr size_t STATS_PER_BATCH_OFFSET = offsetof(BatchStats, max_n);
 
 struct PackParams {
     const uint8_t* queries;

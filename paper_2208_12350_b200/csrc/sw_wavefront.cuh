@@ -48,6 +48,9 @@
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4
 #endif
+#ifndef SW_BODY_BLOCKS
+#define SW_BODY_BLOCKS 1   // 4-column blocks per unrolled loop body (forward)
+#endif
 #ifndef SW_CODE_DIST
 #define SW_CODE_DIST 4     // reference-code prefetch distance in columns
 #endif
@@ -292,7 +295,13 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
         for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_m, sl) + W - 1, stop[sl]));
         T_end = te;
     }
-    for (int t0 = 0; t0 < T_end; t0 += U) {
+    // NB blocks of U columns per loop iteration (the longer body lets ptxas keep loop-carried
+    // values in place); tag bookkeeping stays per U-column block
+    constexpr int NB = REV ? 1 : SW_BODY_BLOCKS;
+    for (int t00 = 0; t00 < T_end; t00 += U * NB) {
+#pragma unroll
+      for (int bb = 0; bb < NB; ++bb) {
+        const int t0 = t00 + bb * U;
         uint32_t nbt = best;  // TAG: running max of this block
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -434,6 +443,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
             T_end = te;
             found_blk = 0;
         }
+      }
     }
     if (!REV && !EV) {
 #pragma unroll
@@ -511,7 +521,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
         }
         // per-half end events are needed only when a shorter reference of the item runs
         // out of pad codes before the sweep ends (see sweep<>, EV)
-        const bool need_ev = !REV && (mmax - mmin > PADR - W - 8);
+        const bool need_ev = !REV && (mmax - mmin > PADR - W - 4 * SW_BODY_BLOCKS - 4);
         const int ns = (nmax + G::ROWS - 1) / G::ROWS;
 
         // this lane's halves

@@ -279,3 +279,34 @@ def test_dpx_peak_probe_runs():
     import torch
     cups = sw.sw_dpx_peak(0, 50.0, torch.cuda.current_stream().cuda_stream)
     assert 1e12 < cups < 5e13
+
+
+def test_host_entry_point_chunked_pipeline(aligner):
+    """The host-buffer entry point splits large batches into overlapped chunks; results must equal
+    the device entry point, and per-pair errors / S = 0 sentinels must survive chunking."""
+    import torch
+    b = synth.generate("c2", 0, 40000)
+    # sprinkle invalid symbols and empty sequences across chunk boundaries
+    pairs = [b.pair(p) for p in range(b.n_pairs)]
+    for p in (0, 9999, 10000, 19999, 20000, 39999):
+        q, r = pairs[p]
+        pairs[p] = (q[:5] + b"N" + q[6:], r) if p % 2 == 0 else (b"", r)
+    b = synth.from_pairs(pairs, synth.DNA_SCORING)
+    ref = aligner.align(b)
+    out = {f: np.zeros(b.n_pairs, np.int32) for f in FIELDS}
+    qa, ra = np.ascontiguousarray(b.queries), np.ascontiguousarray(b.refs)
+    qo, ro = np.ascontiguousarray(b.q_offsets), np.ascontiguousarray(b.r_offsets)
+    st = sw.sw_align_batch_host(aligner.handle, qa.ctypes.data, qo.ctypes.data, ra.ctypes.data, ro.ctypes.data,
+                                b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS},
+                                torch.cuda.current_stream().cuda_stream)
+    assert st == sw.SW_OK
+    for f in FIELDS:
+        np.testing.assert_array_equal(out[f], ref[f])
+    st, nbad = aligner.batch_status()
+    assert st == sw.SW_ERR_BAD_PAIRS and nbad == 3
+    # malformed offsets through the host entry point: every field -1, synchronous error
+    qo_bad = qo.copy(); qo_bad[5] = qo_bad[7] + 1
+    st = sw.sw_align_batch_host(aligner.handle, qa.ctypes.data, qo_bad.ctypes.data, ra.ctypes.data, ro.ctypes.data,
+                                b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS},
+                                torch.cuda.current_stream().cuda_stream)
+    assert st == sw.SW_ERR_INVALID_ARGUMENT and (out["score"] == -1).all()
