@@ -170,6 +170,11 @@ sw_status_t sw_last_launch_count(sw_handle_t h, int32_t* own_kernels, int32_t* l
  * item's longest reference, plus fill/drain). */
 sw_status_t sw_last_cell_counts(sw_handle_t h, int64_t* forward_cells, int64_t* swept_cells);
 
+/* Cells the reverse wavefront of the last batch swept (work items' rows x
+ * columns up to the early stop, incl. fill/drain).  Same synchronisation as
+ * sw_last_cell_counts. */
+sw_status_t sw_last_reverse_cells(sw_handle_t h, int64_t* swept_cells);
+
 /*
  * DPX cell-update roofline probe: runs the minimal
  * s16x2 Gotoh cell-pair mix (3 VIADDMNMX.S16x2 + 1 VIMNMX.S16x2 + 1

@@ -3,7 +3,6 @@
 //   pack -> sort -> forward wavefront -> finish_fwd -> sort -> reverse
 //   wavefront -> finish_rev
 // and the instrumentation entry points.  No exceptions cross the ABI.
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -12,6 +11,7 @@
 #include <vector>
 
 #include "sw.h"
+#include <cub/device/device_radix_sort.cuh>
 #include "sw_common.cuh"
 #include "sw_pack.cuh"
 #include "sw_wavefront.cuh"
@@ -65,14 +65,16 @@ struct sw_context {
     DevBuf<uint32_t> key, key_sorted;
     DevBuf<unsigned long long> keys_fwd, keys_rev;
     // codes
-    DevBuf<uint8_t> qcode, qrev, rcode, rrev;
+    DevBuf<uint8_t> qcode, rcode, rrev;
     // misc
-    DevBuf<uint8_t> cub_temp, scratch;
+    DevBuf<uint8_t> scratch, cub_temp;
     BatchStats* d_stats = nullptr;
     BatchStats* h_stats = nullptr;
     int64_t* h_ext = nullptr;
     int32_t* d_counters = nullptr;  // work-queue heads: 3 forward + 3 reverse routes
     uint32_t* d_sink = nullptr;
+    uint32_t* d_hist = nullptr;     // work-bin histogram [NBINS] (kept zero between passes)
+    uint32_t* d_binbase = nullptr;  // bin cursors [NBINS]
     // host-buffer entry point staging
     DevBuf<uint8_t> st_q, st_r;
     DevBuf<int64_t> st_qo, st_ro;
@@ -159,7 +161,7 @@ sw_status_t check_scoring(sw_context* h, const sw_scoring_t* s, Scoring& sc, boo
     sc.nc = s->alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN;
     sc.max_sigma = smax;
     // s16x2 path: int8 profile of (s - o) in [-127, 127], gap values whose
-    // additions stay inside int16 (values live in [o + e, 32000]).
+    // additions stay inside int16 (shifted values live in [e, 32000]).
     s16_ok = (smax - s->gap_open <= 127) && (smin - s->gap_open >= -127) &&
              s->gap_open >= -8000 && s->gap_extend >= -8000;
     return SW_OK;
@@ -202,6 +204,33 @@ struct HostPlan {
     int32_t route_upper[N_ROUTES];  // pairs per route by lengths alone (>= the device's counts)
     bool reset_cumulative;     // first chunk of a user call
 };
+
+// Order the pairs by work key (h->key), most work first.  Small-region batches
+// (sw_bin.cuh): counting sort on the exact bins pack / finish_fwd histogrammed;
+// otherwise a radix sort of the full 32-bit keys.  Leaves the histogram zero.
+sw_status_t bin_order(sw_context* h, int32_t* order, int64_t n_pairs, bool small, cudaStream_t s) {
+    if (small) {
+        bin_scan_kernel<<<1, BIN_SCAN_THREADS, BIN_SCAN_SMEM, s>>>(h->d_hist, h->d_binbase);
+        const int blocks = (int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 8);
+        bin_scatter_kernel<<<blocks, 256, 0, s>>>(h->key.p, h->d_binbase, order, n_pairs);
+        SW_CUDA(h, cudaGetLastError());
+        h->own_launches += 2;
+        return SW_OK;
+    }
+    SW_CUDA(h, cudaMemsetAsync(h->d_hist, 0, NBINS * sizeof(uint32_t), s));
+    size_t tb = 0;
+    SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p, h->key_sorted.p, h->iota.p, order,
+                                                         (int)n_pairs, 0, 32, s));
+    {
+        sw_status_t e = ensure(h, h->cub_temp, tb);
+        if (e != SW_OK) return e;
+    }
+    tb = h->cub_temp.cap;
+    SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp.p, tb, h->key.p, h->key_sorted.p, h->iota.p, order,
+                                                         (int)n_pairs, 0, 32, s));
+    ++h->lib_launches;
+    return SW_OK;
+}
 
 // The batch pipeline on device pointers.  host_ext (optional) = {q0, qN, r0, rN}.
 sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_off, const uint8_t* refs,
@@ -260,7 +289,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     ENS(nlen, N); ENS(mlen, N); ENS(nlen_rev, N); ENS(mlen_rev, N); ENS(target, N); ENS(iota, N);
     ENS(order, N); ENS(order_rev, N); ENS(qpos, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
     ENS(keys_fwd, N); ENS(keys_rev, N);
-    ENS(qcode, tq + 32); ENS(qrev, tq + 32);
+    ENS(qcode, tq + 32);
     {
         // Every byte of the reference code buffers must be a valid code of the batch's
         // alphabet: finished halves of a work item keep reading past their reference.
@@ -271,12 +300,6 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
             SW_CUDA(h, cudaMemsetAsync(h->rrev.p, 0, h->rrev.cap, s));
             h->codes_alphabet = sc.alphabet;
         }
-    }
-    {
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p, h->key_sorted.p, h->iota.p, h->order.p,
-                                                  (int)N, 0, 32, s);
-        ENS(cub_temp, tb);
     }
 
     const bool protein = sc.alphabet == SW_ALPHABET_PROTEIN;
@@ -293,12 +316,13 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
         P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA) ? 1 : 0;  // TAG route: DNA batches
         P.rows_s16 = rows16; P.rows_s32 = rows32;
-        P.qcode = h->qcode.p; P.rcode = h->rcode.p; P.rrev = h->rrev.p;
+        P.qcode = h->qcode.p; P.rcode = h->rcode.p;
         P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
-        P.iota = h->iota.p; P.stats = h->d_stats;
-        const int64_t warps = std::min<int64_t>(n_pairs, (int64_t)h->sm_count * 64);
-        const int blocks = (int)((warps * 32 + 255) / 256);
-        pack_kernel<<<blocks, 256, 0, s>>>(P);
+        P.hist = h->d_hist; P.keys_fwd = h->keys_fwd.p; P.iota = h->iota.p; P.stats = h->d_stats;
+        // one warp per 32 pairs, at most one full wave of warps
+        const int64_t warps = std::min<int64_t>((n_pairs + 31) / 32, (int64_t)h->sm_count * 64);
+        const int blocks = (int)((warps + PACK_WARPS - 1) / PACK_WARPS);
+        pack_kernel<<<blocks, PACK_WARPS * 32, 0, s>>>(P);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
     }
@@ -316,6 +340,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         hs = *h->h_stats;
     }
     if (hs.malformed) {
+        SW_CUDA(h, cudaMemsetAsync(h->d_hist, 0, NBINS * sizeof(uint32_t), s));  // pack binned some pairs
         fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, n_pairs);
         return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
     }
@@ -334,17 +359,20 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
                                   (const void*)wavefront_kernel<TS32, W32, K32, true, false>};
     Launch lf[N_ROUTES], lr[N_ROUTES];
     for (int r = 0; r < N_ROUTES; ++r) {
-        // reverse-pass pairs are a subset of the forward ones: forward counts bound the grids
+        // reverse-pass pairs are a subset of the forward ones (finish_fwd may move TAG pairs to
+        // S16): forward counts bound the grids
+        const bool demote = (int64_t)sc.max_sigma * hs.max_n > TAG_MAX_SCORE;  // finish_fwd's TAG -> S16 rule
+        const int64_t rev_upper = hs.fwd_count[r] + (r == ROUTE_S16 && demote ? hs.fwd_count[ROUTE_TAG] : 0);
         if (r == ROUTE_S32) {
             lf[r] = plan_wave<G32>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
-            lr[r] = plan_wave<G32>(h, krev[r], sc.nc, hs.fwd_count[r]);
+            lr[r] = plan_wave<G32>(h, krev[r], sc.nc, rev_upper);
         } else if (protein) {
             // 3-warp blocks: 5 blocks x 3 warps fit the SM's shared memory (4-warp blocks: only 3)
             lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], 3);
-            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, hs.fwd_count[r], 3);
+            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, rev_upper, 3);
         } else {
             lf[r] = plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
-            lr[r] = plan_wave<G16>(h, krev[r], sc.nc, hs.fwd_count[r]);
+            lr[r] = plan_wave<G16>(h, krev[r], sc.nc, rev_upper);
         }
     }
 
@@ -365,13 +393,12 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     }
 
     // 5. forward binning (length-sorted, longest first)
-    SW_CUDA(h, cudaMemsetAsync(h->keys_fwd.p, 0, N * sizeof(unsigned long long), s));
-    {
-        size_t tb = h->cub_temp.cap;
-        SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp.p, tb, h->key.p, h->key_sorted.p, h->iota.p,
-                                                             h->order.p, (int)N, 0, 32, s));
-        ++h->lib_launches;
-    }
+    // counting sort when every key is in the small region (sw_bin.cuh): bounded by the extents
+    const int min_rows = std::min(rows16, rows32);
+    const bool small_fwd = hs.max_m < BIN_COLS && (hs.max_n + min_rows - 1) / min_rows <= BIN_MAX_STRIPES;
+    const bool small_rev = small_fwd && (int64_t)sc.max_sigma * std::min(hs.max_n, hs.max_m) < BIN_COLS;
+    st = bin_order(h, h->order.p, n_pairs, small_fwd, s);
+    if (st != SW_OK) return st;
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[3], s));
 
     // 6. forward wavefront
@@ -379,6 +406,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     WaveParams W;
     W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
     W.tag_mul = 64;
+    W.one = 1;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p;
     W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &h->d_stats->swept_fwd; W.counts = h->d_stats->fwd_count;
     for (int r = 0; r < N_ROUTES; ++r) {
@@ -394,28 +422,23 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     // 7. decode forward keys, prepare the reverse pass
     FinishParams F;
     F.n_pairs = n_pairs; F.flags = h->flags.p; F.keys_fwd = h->keys_fwd.p; F.keys_rev = h->keys_rev.p;
-    F.qcode = h->qcode.p; F.qrev = h->qrev.p; F.rcode = h->rcode.p; F.rrev = h->rrev.p;
+    F.rcode = h->rcode.p; F.rrev = h->rrev.p;
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
-    F.target = h->target.p; F.key_rev = h->key.p; F.iota = h->iota.p; F.rows_s16 = rows16; F.rows_s32 = rows32;
-    F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend;
+    F.target = h->target.p; F.key_rev = h->key.p; F.hist = h->d_hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
+    F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
     F.out = *out; F.stats = h->d_stats;
     {
-        const int64_t warps = std::min<int64_t>(n_pairs, (int64_t)h->sm_count * 64);
+        const int64_t warps = std::min<int64_t>((n_pairs + FIN_PPW - 1) / FIN_PPW, (int64_t)h->sm_count * 64);
         finish_fwd_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(F);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
     }
-    SW_CUDA(h, cudaMemsetAsync(h->keys_rev.p, 0, N * sizeof(unsigned long long), s));
-    {
-        size_t tb = h->cub_temp.cap;
-        SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp.p, tb, h->key.p, h->key_sorted.p, h->iota.p,
-                                                             h->order_rev.p, (int)N, 0, 32, s));
-        ++h->lib_launches;
-    }
+    st = bin_order(h, h->order_rev.p, n_pairs, small_rev, s);
+    if (st != SW_OK) return st;
     if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[5], s));
 
     // 8. reverse wavefront on the reversed prefixes
-    W.qcode = h->qrev.p; W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p;
+    W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p;
     W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &h->d_stats->swept_rev; W.counts = h->d_stats->rev_count;
     for (int r = 0; r < N_ROUTES; ++r) {
         if (lr[r].blocks <= 0) continue;
@@ -487,15 +510,19 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
     set_smem_attr(wavefront_kernel<TS16, W16, K16, true, false>, big);
     set_smem_attr(wavefront_kernel<TS32, W32, K32, false, false>, big);
     set_smem_attr(wavefront_kernel<TS32, W32, K32, true, false>, big);
+    set_smem_attr(bin_scan_kernel, BIN_SCAN_SMEM);
     if (cudaMalloc(&h->d_stats, sizeof(BatchStats)) != cudaSuccess ||
         cudaMallocHost(&h->h_stats, sizeof(BatchStats)) != cudaSuccess ||
         cudaMallocHost(&h->h_ext, 4 * sizeof(int64_t)) != cudaSuccess ||
         cudaMalloc(&h->d_counters, 8 * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_hist, NBINS * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_binbase, NBINS * sizeof(uint32_t)) != cudaSuccess) {
         sw_free(h);
         return SW_ERR_OUT_OF_MEMORY;
     }
     cudaMemset(h->d_stats, 0, sizeof(BatchStats));
+    cudaMemset(h->d_hist, 0, NBINS * sizeof(uint32_t));
     for (auto& ev : h->ev) {
         if (cudaEventCreate(&ev) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
     }
@@ -545,8 +572,6 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
 #undef ENS
     // Chunks of about equal cell count; chunk k+1's host-to-device copy (copy stream) overlaps
     // chunk k's kernels (caller's stream), and chunk k's results return while k+1 computes.
-    const bool protein = sc.alphabet == SW_ALPHABET_PROTEIN;
-    const int rows16 = protein ? GP::ROWS : G16::ROWS;
     const bool tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA);
     double total_cells = 0;
     for (int64_t p = 0; p < n_pairs; ++p)
@@ -588,8 +613,8 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
             hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
             if (n == 0 || m == 0) continue;
             const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
-            const int route = (s16_ok && tag_ok && smax <= TAG_MAX_SCORE && n <= rows16) ? ROUTE_TAG
-                            : (s16_ok && smax <= 32000) ? ROUTE_S16 : ROUTE_S32;
+            const int route = (s16_ok && tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
+                            : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
             ++hp.route_upper[route];
         }
         hp.reset_cumulative = k == 0;
@@ -633,14 +658,16 @@ sw_status_t sw_free(sw_handle_t h) {
     cudaDeviceSynchronize();
     release(h->nlen); release(h->mlen); release(h->nlen_rev); release(h->mlen_rev); release(h->target);
     release(h->iota); release(h->order); release(h->order_rev); release(h->qpos); release(h->rpos); release(h->flags);
-    release(h->key); release(h->key_sorted); release(h->keys_fwd); release(h->keys_rev);
-    release(h->qcode); release(h->qrev); release(h->rcode); release(h->rrev); release(h->cub_temp);
+    release(h->key); release(h->key_sorted); release(h->cub_temp); release(h->keys_fwd); release(h->keys_rev);
+    release(h->qcode); release(h->rcode); release(h->rrev);
     release(h->scratch); release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
     if (h->d_stats) cudaFree(h->d_stats);
     if (h->h_stats) cudaFreeHost(h->h_stats);
     if (h->h_ext) cudaFreeHost(h->h_ext);
     if (h->d_counters) cudaFree(h->d_counters);
     if (h->d_sink) cudaFree(h->d_sink);
+    if (h->d_hist) cudaFree(h->d_hist);
+    if (h->d_binbase) cudaFree(h->d_binbase);
     for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
     for (int k = 0; k < 8; ++k) {
         if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
@@ -707,6 +734,14 @@ sw_status_t sw_last_cell_counts(sw_handle_t h, int64_t* fwd, int64_t* swept) {
     SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
     if (fwd) *fwd = (int64_t)h->h_stats->cells;
     if (swept) *swept = (int64_t)h->h_stats->swept_fwd;
+    return SW_OK;
+}
+
+sw_status_t sw_last_reverse_cells(sw_handle_t h, int64_t* swept) {
+    if (!h || !swept) return SW_ERR_INVALID_ARGUMENT;
+    if (h->have_last) SW_CUDA(h, cudaStreamSynchronize(h->last_stream));
+    SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
+    *swept = (int64_t)h->h_stats->swept_rev;
     return SW_OK;
 }
 

@@ -15,6 +15,8 @@ constexpr uint32_t FULL = 0xffffffffu;
 // checks" lesson, reused here).
 constexpr int PADL = 32;
 constexpr int PADR = 64;
+// Pad codes finish_fwd writes right after each reversed prefix (<= PADR).
+constexpr int REV_PAD = 16;
 // Tail guard of the code buffers: a work item's shorter half keeps reading
 // (frozen, harmless) codes up to the item's longest reference + fill/drain.
 constexpr int64_t GUARD = SW_MAX_SEQ_LEN + 256;
@@ -29,6 +31,8 @@ constexpr uint8_t CODE_BAD = 0xff;
 //   ROUTE_S16  s16x2 lanes, improvement columns saved to shared memory
 //   ROUTE_S32  int32 lanes (scorings / lengths that are not int16-safe)
 constexpr int ROUTE_TAG = 0, ROUTE_S16 = 1, ROUTE_S32 = 2, N_ROUTES = 3;
+// s16 lanes hold Hb = H - o; the int8 profile already forces -o <= 126 (s - o <= 127, s >= 1)
+constexpr int S16_MAX_SCORE = 32000;  // Hb <= 32126 < 32768
 constexpr int TAG_MAX_SCORE = 511;    // 511 * 64 + 63 < 32768 (6 tag bits: column-in-block, row)
 // Work keys: [31:30] 3 - route (0 = trivial / invalid), [29:16] stripes, [15:0] columns
 __host__ __device__ constexpr uint32_t route_key(int route) { return (uint32_t)(3 - route) << 30; }
@@ -99,6 +103,8 @@ struct TS16 {
     using V = uint32_t;
     static constexpr int NH = 2;
     static __device__ __forceinline__ V splat(int x) { return (uint32_t)(x & 0xffff) * 0x10001u; }
+    // 32-bit addend that adds x to both halves of a word whose low half + x stays >= 0
+    static __device__ __forceinline__ V lift(int x) { return (uint32_t)(x * 65537); }
     static __device__ __forceinline__ V add(V a, V b) { return __vadd2(a, b); }
     // max(a + b, c)
     static __device__ __forceinline__ V addmax(V a, V b, V c) { return __viaddmax_s16x2(a, b, c); }
@@ -124,6 +130,7 @@ struct TS32 {
     using V = uint32_t;  // holds int32 bits
     static constexpr int NH = 1;
     static __device__ __forceinline__ V splat(int x) { return (uint32_t)x; }
+    static __device__ __forceinline__ V lift(int x) { return (uint32_t)x; }
     static __device__ __forceinline__ V add(V a, V b) { return (uint32_t)((int)a + (int)b); }
     static __device__ __forceinline__ V addmax(V a, V b, V c) { return (uint32_t)__viaddmax_s32((int)a, (int)b, (int)c); }
     static __device__ __forceinline__ V max_relu(V a, V b) { return (uint32_t)__vimax_s32_relu((int)a, (int)b); }

@@ -4,6 +4,7 @@
 #pragma once
 #include "sw_common.cuh"
 #include "sw_pack.cuh"
+#include "sw_bin.cuh"
 
 namespace swb {
 
@@ -11,9 +12,7 @@ struct FinishParams {
     int64_t n_pairs;
     const uint8_t* flags;
     const unsigned long long* keys_fwd;
-    const unsigned long long* keys_rev;
-    const uint8_t* qcode;
-    uint8_t* qrev;
+    unsigned long long* keys_rev;   // reverse argmax keys: zeroed by finish_fwd
     const uint8_t* rcode;
     uint8_t* rrev;
     const int64_t* qpos;
@@ -21,10 +20,11 @@ struct FinishParams {
     int32_t* nlen_rev;
     int32_t* mlen_rev;
     int32_t* target;
-    uint32_t* key_rev;
-    int32_t* iota;
+    uint32_t* key_rev;              // reverse work key per pair (0: no reverse work)
+    uint32_t* hist;                 // bin histogram (zero on entry)
     int rows_s16, rows_s32;
     int max_sigma, gap_extend;
+    uint8_t pad_code;
     sw_result_t out;
     BatchStats* stats;
 };
@@ -36,9 +36,16 @@ __device__ __forceinline__ void decode_key(unsigned long long key, int& S, int& 
 }
 
 // After the forward pass: score / q_end / r_end into the caller's arrays,
-// sentinels for invalid and S = 0 pairs, and the reversed prefixes
-// reverse(q[0..q_end]) x reverse(r[0..r_end]) materialised for the reverse
-// pass (reading R6).  One warp per pair.
+// sentinels for invalid and S = 0 pairs, and the reversed reference prefix
+// reverse(r[0..r_end]) materialised for the reverse pass (reading R6; the
+// reverse pass reads the query prefix backwards in place).  A warp takes
+// FIN_PPW consecutive pairs: lanes < FIN_PPW decode one pair each, then the
+// warp writes the pairs' reversed prefixes as one flat list of aligned 32-bit
+// words (every word = one PRMT of two aligned source words), so the loads of
+// all its pairs are in flight together.
+constexpr int FIN_PPW = 8;
+constexpr int FIN_FB = 4;   // words per lane loaded before any is stored
+
 __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     __shared__ int s_route[N_ROUTES];
     if (threadIdx.x < N_ROUTES) s_route[threadIdx.x] = 0;
@@ -47,57 +54,115 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     int l_route[N_ROUTES] = {0, 0, 0};
-    for (int64_t p = gw; p < P.n_pairs; p += nw) {
-        const uint8_t fl = P.flags[p];
-        const unsigned long long key = P.keys_fwd[p];
-        int S = 0, j = -1, i = -1;
-        if (key) decode_key(key, S, j, i);
-        if (fl & FLAG_BAD) {
-            if (lane == 0) {
+    const uint32_t padw = (uint32_t)P.pad_code * 0x01010101u;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(P.rcode);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(P.rrev);
+    for (int64_t base = gw * FIN_PPW; base < P.n_pairs; base += nw * FIN_PPW) {
+        const int64_t p = base + lane;
+        int64_t rp = 0, w0 = 0;
+        int j = -1, cnt = 0;
+        if (lane < FIN_PPW && p < P.n_pairs) {
+            P.keys_rev[p] = 0ull;
+            const uint8_t fl = P.flags[p];
+            const unsigned long long key = P.keys_fwd[p];
+            int S = 0, i = -1;
+            if (key) decode_key(key, S, j, i);
+            if (fl & FLAG_BAD) {
                 P.out.score[p] = -1; P.out.q_end[p] = -1; P.out.r_end[p] = -1;
                 P.out.q_start[p] = -1; P.out.r_start[p] = -1;
-                P.key_rev[p] = 0; P.iota[p] = (int32_t)p;
-            }
-            continue;
-        }
-        if (S == 0) {
-            if (lane == 0) {
+                P.key_rev[p] = 0;
+            } else if (S == 0) {
                 P.out.score[p] = 0; P.out.q_end[p] = -1; P.out.r_end[p] = -1;
                 P.out.q_start[p] = -1; P.out.r_start[p] = -1;
-                P.key_rev[p] = 0; P.iota[p] = (int32_t)p;
+                P.key_rev[p] = 0;
+            } else {
+                P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
+                const int n2 = i + 1;
+                // Columns the reverse pass can need (reading R6): every score-S alignment in the
+                // reversed rectangle starts at its origin (SURVEY.md 8(c) C-5 proof) and spans
+                // M + I columns, M <= n2 aligned pairs and I gap columns each costing >= |e|, so
+                // S <= max_s*M - |e|*I  =>  columns <= n2 + (max_s*n2 - S) / |e|.  Exact bound.
+                int m2 = j + 1;
+                if (P.gap_extend < 0) {
+                    const long long bound = (long long)n2 + ((long long)P.max_sigma * n2 - S) / (long long)(-P.gap_extend);
+                    if (bound < m2) m2 = (int)max(bound, 1LL);
+                }
+                int route = flag_route(fl);
+                // TAG reverse items need H <= 511 in every swept cell, also past the rectangle
+                if (route == ROUTE_TAG && (long long)P.max_sigma * n2 > TAG_MAX_SCORE) route = ROUTE_S16;
+                const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
+                const uint32_t stripes = (uint32_t)((n2 + rows - 1) / rows);
+                P.nlen_rev[p] = n2;
+                P.mlen_rev[p] = m2;
+                P.target[p] = S;
+                // reverse work items are grouped by (stripes, S): the early-stopped sweep's length
+                // follows the alignment's span, for which S is the available proxy
+                const uint32_t key = work_key(route, stripes, (uint32_t)S);
+                P.key_rev[p] = key;
+                const uint32_t bin = key_bin(key);
+                if (bin) atomicAdd(P.hist + bin, 1u);
+                ++l_route[route];
+                // output words covering rrev[rp - PADL .. rp + j + REV_PAD]: PADL pad codes (the
+                // reverse sweep's fill columns), the reversed prefix, then REV_PAD pad codes
+                rp = P.rpos[p];
+                w0 = (rp - PADL) >> 2;
+                cnt = (int)(((rp + j + REV_PAD) >> 2) - w0 + 1);
             }
-            continue;
         }
-        const int64_t qp = P.qpos[p];
-        const int64_t rp = P.rpos[p];
-        for (int k = lane; k <= i; k += 32) P.qrev[qp + k] = P.qcode[qp + i - k];
-        for (int k = lane; k <= j; k += 32) P.rrev[rp + k] = P.rcode[rp + j - k];
-        if (lane == 0) {
-            P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
-            const int n2 = i + 1;
-            // Columns the reverse pass can need (reading R6): every score-S alignment in the
-            // reversed rectangle starts at its origin (SURVEY.md 8(c) C-5 proof) and spans
-            // M + I columns, M <= n2 aligned pairs and I gap columns each costing >= |e|, so
-            // S <= max_s*M - |e|*I  =>  columns <= n2 + (max_s*n2 - S) / |e|.  Exact bound.
-            int m2 = j + 1;
-            if (P.gap_extend < 0) {
-                const long long bound = (long long)n2 + ((long long)P.max_sigma * n2 - S) / (long long)(-P.gap_extend);
-                if (bound < m2) m2 = (int)max(bound, 1LL);
+        // flat list of the warp's words: inclusive scan of the per-pair word counts
+        int incl = cnt;
+#pragma unroll
+        for (int d = 1; d < FIN_PPW; d <<= 1) {
+            const int t = __shfl_up_sync(FULL, incl, d);
+            if (lane >= d) incl += t;
+        }
+        const int excl = incl - cnt;
+        const int total = __shfl_sync(FULL, incl, FIN_PPW - 1);
+        for (int g0 = 0; g0 < total; g0 += 32 * FIN_FB) {
+            uint32_t x0[FIN_FB], x1[FIN_FB], sel[FIN_FB];
+            int64_t aa[FIN_FB], kk0[FIN_FB];
+            int jj[FIN_FB];
+#pragma unroll
+            for (int u = 0; u < FIN_FB; ++u) {
+                const int g = g0 + u * 32 + lane;
+                // owner pair: the last lane whose first word is <= g
+                int own = 0;
+#pragma unroll
+                for (int st = FIN_PPW / 2; st >= 1; st >>= 1) {
+                    const int e = __shfl_sync(FULL, excl, own + st);
+                    if (e <= g) own += st;
+                }
+                const int64_t orp = __shfl_sync(FULL, rp, own);
+                const int64_t ow0 = __shfl_sync(FULL, w0, own);
+                const int oj = __shfl_sync(FULL, j, own);
+                const int oex = __shfl_sync(FULL, excl, own);
+                const int64_t a = (ow0 + (g - oex)) * 4;  // rrev index of the word's byte 0
+                // byte b of the word is rrev[a + b] = rcode[2 rp + j - a - b] (k = a + b - rp)
+                const int64_t sbeg = 2 * orp + oj - a - 3;  // lowest source index (byte 3)
+                const uint32_t o = (uint32_t)(sbeg & 3);
+                aa[u] = a; kk0[u] = a - orp; jj[u] = oj;
+                sel[u] = (o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12);
+                x0[u] = 0; x1[u] = 0;
+                if (g < total) {
+                    x0[u] = __ldg(src + (sbeg >> 2));
+                    x1[u] = __ldg(src + (sbeg >> 2) + 1);
+                }
             }
-            const int route = flag_route(fl);
-            const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
-            const uint32_t stripes = min((n2 + rows - 1) / rows, 0x3fff);
-            P.nlen_rev[p] = n2;
-            P.mlen_rev[p] = m2;
-            P.target[p] = S;
-            // reverse work items are grouped by S: the early-stopped sweep's length follows the
-            // alignment's span, for which S is the available proxy
-            P.key_rev[p] = route_key(route) | (stripes << 16) | (uint32_t)min(S, 0xffff);
-            P.iota[p] = (int32_t)p;
-            ++l_route[route];
+#pragma unroll
+            for (int u = 0; u < FIN_FB; ++u) {
+                if (g0 + u * 32 + lane >= total) continue;
+                uint32_t v = __byte_perm(x0[u], x1[u], sel[u]);
+                const int64_t k0 = kk0[u];
+                if (k0 < 0 || k0 + 3 > jj[u]) {  // first / last words: bytes outside [0, j] are pads
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if (k0 + b < 0 || k0 + b > jj[u]) v = (v & ~(0xffu << (8 * b))) | (padw & (0xffu << (8 * b)));
+                }
+                dst[aa[u] >> 2] = v;
+            }
         }
     }
-    if (lane == 0)
+    if (lane < FIN_PPW)
         for (int r = 0; r < N_ROUTES; ++r)
             if (l_route[r]) atomicAdd(&s_route[r], l_route[r]);
     __syncthreads();

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstddef>
 #include "sw_common.cuh"
+#include "sw_bin.cuh"
 
 namespace swb {
 
@@ -40,14 +41,15 @@ struct PackParams {
     int rows_s16, rows_s32;      // rows per stripe of each path
     uint8_t* qcode;              // [qN - q0]
     uint8_t* rcode;              // padded layout
-    uint8_t* rrev;               // padded layout (pads only here)
     int32_t* nlen;
     int32_t* mlen;
     int64_t* qpos;
     int64_t* rpos;
     uint8_t* flags;
-    uint32_t* key;
-    int32_t* iota;
+    uint32_t* key;               // work key per pair (sw_bin.cuh; 0: no forward work)
+    int32_t* iota;               // 0..n-1 (values of the radix-sort path)
+    uint32_t* hist;              // bin histogram (zero on entry)
+    unsigned long long* keys_fwd;  // forward argmax keys: zeroed here
     BatchStats* stats;
 };
 
@@ -81,51 +83,71 @@ __device__ __forceinline__ uint32_t conv4(uint32_t w, const uint8_t* lut, uint32
     return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
 }
 
-// Convert one sequence: src and dst have the same address mod 16 (by construction of
-// the code-buffer positions), so the body moves as aligned 16-byte vectors.
-// Returns true if a symbol is outside the alphabet; such symbols become `bad_to`.
-__device__ __forceinline__ bool convert_run(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int64_t len,
-                                            const uint8_t* lut, uint8_t bad_to, int lane) {
-    uint32_t badmask = 0;
-    bool bad = false;
-    const int head = (int)(len < (int64_t)((16 - ((uintptr_t)src & 15)) & 15) ? len : (int64_t)((16 - ((uintptr_t)src & 15)) & 15));
-    if (lane < head) {
-        const uint8_t c = lut[src[lane]];
-        bad |= c == CODE_BAD;
-        dst[lane] = c == CODE_BAD ? bad_to : c;
-    }
-    const int64_t body = (len - head) >> 4;
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
-    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-    for (int64_t k = lane; k < body; k += 32) {
-        const uint4 v = __ldg(s4 + k);
-        uint32_t bm = 0;
-        uint4 o;
-        o.x = conv4(v.x, lut, bm); o.y = conv4(v.y, lut, bm); o.z = conv4(v.z, lut, bm); o.w = conv4(v.w, lut, bm);
-        if (bm & 0x80u) {  // rare: replace bad bytes
-            uint32_t* ow = &o.x;
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-                for (int b = 0; b < 4; ++b)
-                    if (((ow[q] >> (8 * b)) & 0xff) == CODE_BAD) ow[q] = (ow[q] & ~(0xffu << (8 * b))) | ((uint32_t)bad_to << (8 * b));
-        }
-        badmask |= bm;
-        d4[k] = o;
-    }
-    const int64_t t0 = head + body * 16;
-    if (lane < len - t0) {
-        const uint8_t c = lut[src[t0 + lane]];
-        bad |= c == CODE_BAD;
-        dst[t0 + lane] = c == CODE_BAD ? bad_to : c;
-    }
-    return bad || (badmask & 0x80u);
+// Byte-wise conversion of one code position (partial vectors at span edges).
+__device__ __forceinline__ uint8_t conv1(uint8_t ch, const uint8_t* lut, uint8_t bad_to, bool& bad) {
+    const uint8_t c = lut[ch];
+    if (c == CODE_BAD) { bad = true; return bad_to; }
+    return c;
 }
 
-__global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
+// 16 bytes -> codes; CODE_BAD (0xff) bytes stay 0xff (bit 7 marks them: valid codes are < 25).
+__device__ __forceinline__ uint4 conv16_raw(uint4 v, const uint8_t* lut) {
+    uint32_t bm = 0;
+    return make_uint4(conv4(v.x, lut, bm), conv4(v.y, lut, bm), conv4(v.z, lut, bm), conv4(v.w, lut, bm));
+}
+
+// Byte mask of bytes [lo, hi) (0 <= lo <= hi <= 16) within 32-bit word q of a 16-byte vector.
+__device__ __forceinline__ uint32_t byte_range_mask(int lo, int hi, int q) {
+    const int a = min(max(lo - 4 * q, 0), 4), b = min(max(hi - 4 * q, 0), 4);
+    const uint32_t mb = b >= 4 ? 0xffffffffu : ((1u << (8 * b)) - 1u);
+    const uint32_t ma = a >= 4 ? 0xffffffffu : ((1u << (8 * a)) - 1u);
+    return mb & ~ma;
+}
+
+// Largest k in [0, cnt) with a[k] <= x (a non-decreasing; k = 0 if none).
+__device__ __forceinline__ int owner_of(const int64_t* a, int cnt, int64_t x) {
+    int lo = 0, hi = cnt - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ void store16_within(uint8_t* dst, int64_t y0, uint4 v, int64_t lo, int64_t hi) {
+    if (y0 >= lo && y0 + 16 <= hi) {
+        *reinterpret_cast<uint4*>(dst + y0) = v;
+    } else {  // span edge: only this warp's bytes (the neighbour warp writes the others)
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (y0 + b >= lo && y0 + b < hi) dst[y0 + b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+    }
+}
+
+constexpr int PACK_WARPS = 8;  // warps per pack block (256 threads)
+constexpr int PACK_PPW = 8;    // pairs per warp
+constexpr int PACK_FB = 4;     // 16-byte vectors per lane in flight
+
+// One warp packs PACK_PPW consecutive pairs: lanes read the pairs' offsets,
+// then the warp converts the pairs' reference and query payloads as flat
+// lists of aligned 16-byte output vectors (the code buffers keep the payloads'
+// 16-byte phase), PACK_FB vectors per lane loaded before any is stored.  The
+// reference layout gives every pair the slot [rp - PADL, rp + m + PADR): pad
+// codes around the converted reference; references are >= PADL + PADR apart,
+// so a vector holds bytes of at most one reference plus pads (one load and a
+// byte mask).  Vectors shared with the neighbouring warp's span are written
+// byte-wise (only this warp's bytes).
+__global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
+    constexpr int PPW = PACK_PPW;
     __shared__ int s_bad, s_route[N_ROUTES], s_maxn, s_maxm, s_malformed;
     __shared__ unsigned long long s_cells;
     __shared__ uint8_t lut[256];
+    __shared__ int64_t s_slot[PACK_WARPS][PPW];   // rcode slot start rp - PADL
+    __shared__ int64_t s_rdelta[PACK_WARPS][PPW]; // ra - rp: payload index of code position y is y + delta
+    __shared__ int32_t s_m[PACK_WARPS][PPW];
+    __shared__ int64_t s_qa[PACK_WARPS][PPW];     // query payload starts
+    __shared__ uint32_t s_badbits[PACK_WARPS];
     if (threadIdx.x == 0) {
         s_bad = s_maxn = s_maxm = s_malformed = 0;
         for (int r = 0; r < N_ROUTES; ++r) s_route[r] = 0;
@@ -134,32 +156,149 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
     for (int c = threadIdx.x; c < 256; c += blockDim.x) lut[c] = ascii_code(P.alphabet, c);
     __syncthreads();
     const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint8_t pad_code = (uint8_t)((P.alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN) - 1);
+    const uint32_t padw = (uint32_t)pad_code * 0x01010101u;
     int l_bad = 0, l_route[N_ROUTES] = {0, 0, 0}, l_maxn = 0, l_maxm = 0, l_malf = 0;
     unsigned long long l_cells = 0;
-    for (int64_t p = gw; p < P.n_pairs; p += nw) {
-        const int64_t qa = P.q_off[p], qb = P.q_off[p + 1];
-        const int64_t ra = P.r_off[p], rb = P.r_off[p + 1];
+    int64_t* slot = s_slot[wib];
+    int64_t* rdelta = s_rdelta[wib];
+    int32_t* sm = s_m[wib];
+    int64_t* sqa = s_qa[wib];
+    for (int64_t base = gw * PPW; base < P.n_pairs; base += nw * PPW) {
+        const int cnt = (int)(P.n_pairs - base < PPW ? P.n_pairs - base : (int64_t)PPW);
+        const int64_t p = base + lane;
+        const bool act = lane < cnt;
+        int64_t qa = 0, qb = 0, ra = 0, rb = 0;
+        if (act) { qa = P.q_off[p]; qb = P.q_off[p + 1]; ra = P.r_off[p]; rb = P.r_off[p + 1]; }
         const int64_t n = qb - qa, m = rb - ra;
-        bool in_range = qa >= P.q0 && qb <= P.qN && ra >= P.r0 && rb <= P.rN && n >= 0 && m >= 0;
-        if (n < 0 || m < 0) l_malf = 1;
-        bool bad = !in_range || n > SW_MAX_SEQ_LEN || m > SW_MAX_SEQ_LEN;
+        const bool malf = act && (n < 0 || m < 0 || qa < P.q0 || qb > P.qN || ra < P.r0 || rb > P.rN);
+        if (malf) l_malf = 1;
         const int64_t qp = (qa - P.q0) + P.qshift;
         const int64_t rp = (ra - P.r0) + (p + 1) * PADL + p * PADR + P.rshift;
-        if (in_range && !bad) {
-            bad |= convert_run(P.queries + qa, P.qcode + qp, n, lut, pad_code, lane);
-            bad |= convert_run(P.refs + ra, P.rcode + rp, m, lut, pad_code, lane);
-            // pads around the reference, in both the forward and the reverse buffer
-            for (int k = lane; k < PADL + PADR; k += 32) {
-                const int64_t pos = k < PADL ? rp - PADL + k : rp + m + (k - PADL);
-                P.rcode[pos] = pad_code;
-                P.rrev[pos] = pad_code;
+        if (lane == 0) s_badbits[wib] = 0u;
+        if (!__any_sync(FULL, malf)) {
+            if (act) { slot[lane] = rp - PADL; rdelta[lane] = ra - rp; sm[lane] = (int32_t)m; sqa[lane] = qa; }
+            __syncwarp();
+            uint32_t badbits = 0;
+            // ---- references: output vectors of [lo, hi) in rcode ----
+            const int64_t lo = __shfl_sync(FULL, rp, 0) - PADL;
+            const int64_t hi = __shfl_sync(FULL, rp + m + PADR, cnt - 1);
+            const int64_t v_lo = lo >> 4, v_hi = (hi - 1) >> 4;
+            for (int64_t vb = v_lo; vb <= v_hi; vb += 32 * PACK_FB) {
+                uint4 src[PACK_FB];
+                int rs[PACK_FB], re[PACK_FB], kk[PACK_FB];
+#pragma unroll
+                for (int u = 0; u < PACK_FB; ++u) {
+                    const int64_t y0 = (vb + u * 32 + lane) * 16;
+                    src[u] = make_uint4(0, 0, 0, 0);
+                    rs[u] = 0; re[u] = 0; kk[u] = 0;
+                    if (vb + u * 32 + lane > v_hi) continue;
+                    const int k = owner_of(slot, cnt, y0);
+                    const int64_t rk = slot[k] + PADL, ek = rk + sm[k];
+                    const int64_t a = max(y0, rk), b = min(y0 + 16, ek);
+                    kk[u] = k;
+                    if (a < b) {
+                        rs[u] = (int)(a - y0); re[u] = (int)(b - y0);
+                        const int64_t s0 = y0 + rdelta[k];  // payload index of the vector's byte 0 (16-aligned address)
+                        if (s0 >= P.r0 && s0 + 16 <= P.rN) {  // whole block inside the caller's payload
+                            src[u] = __ldg(reinterpret_cast<const uint4*>(P.refs + s0));
+                        } else {
+                            uint32_t w[4] = {0, 0, 0, 0};
+                            for (int bb = rs[u]; bb < re[u]; ++bb) w[bb >> 2] |= (uint32_t)P.refs[s0 + bb] << (8 * (bb & 3));
+                            src[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PACK_FB; ++u) {
+                    if (vb + u * 32 + lane > v_hi) continue;
+                    const int64_t y0 = (vb + u * 32 + lane) * 16;
+                    uint4 o = make_uint4(padw, padw, padw, padw);
+                    if (rs[u] == 0 && re[u] == 16) {  // common case: the whole vector is reference bytes
+                        uint32_t bm = 0;
+                        o = make_uint4(conv4(src[u].x, lut, bm), conv4(src[u].y, lut, bm), conv4(src[u].z, lut, bm),
+                                       conv4(src[u].w, lut, bm));
+                        if (bm & 0x80u) {
+                            badbits |= 1u << kk[u];
+                            auto fix = [&](uint32_t w) {
+                                const uint32_t bb = ((w & 0x80808080u) >> 7) * 0xffu;
+                                return (w & ~bb) | (padw & bb);
+                            };
+                            o = make_uint4(fix(o.x), fix(o.y), fix(o.z), fix(o.w));
+                        }
+                    } else if (re[u] > rs[u]) {
+                        const uint4 c = conv16_raw(src[u], lut);
+                        const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
+                        uint32_t ow[4];
+                        uint32_t badacc = 0;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t rm = byte_range_mask(rs[u], re[u], q);
+                            const uint32_t bb = ((cw[q] & 0x80808080u) >> 7) * 0xffu & rm;  // bad bytes of the reference
+                            badacc |= bb;
+                            const uint32_t keep = rm & ~bb;
+                            ow[q] = (cw[q] & keep) | (padw & ~keep);
+                        }
+                        if (badacc) badbits |= 1u << kk[u];
+                        o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+                    }
+                    store16_within(P.rcode, y0, o, lo, hi);
+                }
             }
+            // ---- queries: output vectors of [qlo, qhi) in qcode (no pads; shift qshift - q0) ----
+            const int64_t qlo = __shfl_sync(FULL, qa, 0) - P.q0 + P.qshift;
+            const int64_t qhi = __shfl_sync(FULL, qb, cnt - 1) - P.q0 + P.qshift;
+            const int64_t qd = P.q0 - P.qshift;  // payload index of code position y is y + qd
+            if (qhi > qlo) {
+                const int64_t qv_hi = (qhi - 1) >> 4;
+                for (int64_t vb = qlo >> 4; vb <= qv_hi; vb += 32 * PACK_FB) {
+                    uint4 src[PACK_FB];
+#pragma unroll
+                    for (int u = 0; u < PACK_FB; ++u) {
+                        const int64_t y0 = (vb + u * 32 + lane) * 16;
+                        src[u] = make_uint4(0, 0, 0, 0);
+                        if (vb + u * 32 + lane > qv_hi) continue;
+                        if (y0 >= qlo && y0 + 16 <= qhi) {
+                            src[u] = __ldg(reinterpret_cast<const uint4*>(P.queries + y0 + qd));
+                        } else {  // span edge: only bytes inside [qlo, qhi)
+                            uint32_t w[4] = {0, 0, 0, 0};
+                            for (int bb = 0; bb < 16; ++bb)
+                                if (y0 + bb >= qlo && y0 + bb < qhi) w[bb >> 2] |= (uint32_t)P.queries[y0 + qd + bb] << (8 * (bb & 3));
+                            src[u] = make_uint4(w[0], w[1], w[2], w[3]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < PACK_FB; ++u) {
+                        if (vb + u * 32 + lane > qv_hi) continue;
+                        const int64_t y0 = (vb + u * 32 + lane) * 16;
+                        uint32_t bm = 0;
+                        uint32_t cw[4] = {conv4(src[u].x, lut, bm), conv4(src[u].y, lut, bm), conv4(src[u].z, lut, bm),
+                                          conv4(src[u].w, lut, bm)};
+                        if (bm & 0x80u) {
+                        const int lo16 = qlo - y0 > 0 ? (int)(qlo - y0) : 0, hi16 = qhi - y0 < 16 ? (int)(qhi - y0) : 16;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint32_t bb = ((cw[q] & 0x80808080u) >> 7) * 0xffu & byte_range_mask(lo16, hi16, q);
+                            if (bb) {  // rare: attribute each bad byte to its pair, store pads instead
+                                for (int b = 0; b < 4; ++b)
+                                    if ((bb >> (8 * b)) & 0xffu) badbits |= 1u << owner_of(sqa, cnt, y0 + qd + 4 * q + b);
+                                cw[q] = (cw[q] & ~bb) | (padw & bb);
+                            }
+                        }
+                        }
+                        store16_within(P.qcode, y0, make_uint4(cw[0], cw[1], cw[2], cw[3]), qlo, qhi);
+                    }
+                }
+            }
+            if (badbits) atomicOr(&s_badbits[wib], badbits);
+            __syncwarp();
         }
-        bad = __any_sync(FULL, bad);
-        if (lane == 0) {
+        // ---- per-pair metadata (lane = pair) ----
+        if (act) {
+            const bool bad = malf || n > SW_MAX_SEQ_LEN || m > SW_MAX_SEQ_LEN || ((s_badbits[wib] >> lane) & 1u);
             uint32_t key = 0;
             uint8_t fl = 0;
             int nn = 0, mm = 0;
@@ -171,12 +310,13 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
                 // largest score the pair can reach (reading R13): picks the lane width
                 const int64_t smax = (int64_t)P.max_sigma * (int64_t)min(nn, mm);
                 const int route = (P.s16_ok && P.tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
-                                : (P.s16_ok && smax <= 32000) ? ROUTE_S16 : ROUTE_S32;
+                                : (P.s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
                 fl = route_flag(route);
                 if (nn > 0 && mm > 0) {
                     const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
-                    const uint32_t stripes = min((nn + rows - 1) / rows, 0x3fff);
-                    key = route_key(route) | (stripes << 16) | (uint32_t)mm;
+                    key = work_key(route, (uint32_t)((nn + rows - 1) / rows), (uint32_t)mm);
+                    const uint32_t bin = key_bin(key);
+                    if (bin) atomicAdd(P.hist + bin, 1u);
                     ++l_route[route];
                     l_cells += (unsigned long long)nn * (unsigned long long)mm;
                 }
@@ -190,17 +330,18 @@ __global__ void __launch_bounds__(256) pack_kernel(PackParams P) {
             P.flags[p] = fl;
             P.key[p] = key;
             P.iota[p] = (int32_t)p;
+            P.keys_fwd[p] = 0ull;
         }
+        __syncwarp();
     }
-    if (lane == 0) {
-        if (l_bad) atomicAdd(&s_bad, l_bad);
-        for (int r = 0; r < N_ROUTES; ++r)
-            if (l_route[r]) atomicAdd(&s_route[r], l_route[r]);
-        if (l_maxn) atomicMax(&s_maxn, l_maxn);
-        if (l_maxm) atomicMax(&s_maxm, l_maxm);
-        if (l_malf) atomicOr(&s_malformed, 1);
-        if (l_cells) atomicAdd(&s_cells, l_cells);
-    }
+    // block reduction of the lanes' statistics
+    if (l_bad) atomicAdd(&s_bad, l_bad);
+    for (int r = 0; r < N_ROUTES; ++r)
+        if (l_route[r]) atomicAdd(&s_route[r], l_route[r]);
+    if (l_maxn) atomicMax(&s_maxn, l_maxn);
+    if (l_maxm) atomicMax(&s_maxm, l_maxm);
+    if (l_malf) atomicOr(&s_malformed, 1);
+    if (l_cells) atomicAdd(&s_cells, l_cells);
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_bad) atomicAdd(&P.stats->n_bad, s_bad);

@@ -1,15 +1,20 @@
 // sw_wavefront.cuh -- steps a3 (forward: score + end) and a4 (reverse: start)
 // of SURVEY.md sec. 8(a): the anti-diagonal Gotoh wavefront on sm_100a.
 //
-// Recurrence (affine state PAPER.md:507/713-714), written
-// in the "HO" form the kernel keeps in registers (HO = H + gap_open):
-//   E[i][j]  = max(E[i][j-1] + e, HO[i][j-1])                 VIADDMNMX
-//   F[i][j]  = max(F[i-1][j] + e, HO[i-1][j])                 VIADDMNMX
-//   H[i][j]  = max(HO[i-1][j-1] + (s(q_i, r_j) - o),
-//                  max(E, F, 0))                               VIMNMX.RELU + VIADDMNMX
-//   HO[i][j] = H[i][j] + o                                     VIADD
-// which is the plain recurrence with E/F relu-clamped and -inf borders
-// replaced by gap_open (pin P13, reading R13).
+// Recurrence (affine state PAPER.md:507/713-714).  The
+// kernel keeps E and F shifted by -o (o = gap_open < 0) and H both plain and
+// shifted, so every value stays >= 0 and the "+ o" step is a plain 32-bit add
+// (IMAD on the FMA pipe: no borrow crosses the 16-bit halves) instead of a
+// DPX add on the integer ALU pipe:
+//   Eb[i][j] = max(Eb[i][j-1] + e, H[i][j-1])                 VIADDMNMX
+//   Fb[i][j] = max(Fb[i-1][j] + e, H[i-1][j])                 VIADDMNMX
+//   t        = max(Eb, Fb, -o)                                VIMNMX3
+//   Hb[i][j] = max(H[i-1][j-1] + (s(q_i, r_j) - o), t)        VIADDMNMX
+//   H[i][j]  = Hb[i][j] + o                                   IMAD
+// with Eb = E - o, Fb = F - o, Hb = H - o; this is the plain recurrence
+// H = max(H[i-1][j-1] + s, E, F, 0), E = max(E[i][j-1] + e, H[i][j-1] + o),
+// F = max(F[i-1][j] + e, H[i-1][j] + o), with E/F relu-clamped at o and the
+// -inf borders replaced by gap_open (pin P13, reading R13).
 //
 // Layout (B200-first, not ADEPT's block-per-pair / thread-per-residue):
 // * a warp is split into 32/W segments of W lanes; a segment owns one (s32)
@@ -39,12 +44,6 @@
 #include "sw_common.cuh"
 #include "sw_pack.cuh"
 
-#ifndef SW_CELL_V2
-#define SW_CELL_V2 0
-#endif
-#ifndef SW_CELL_V3
-#define SW_CELL_V3 0
-#endif
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4
 #endif
@@ -67,7 +66,7 @@
 namespace swb {
 
 struct WaveParams {
-    const uint8_t* qcode;       // query codes (positions qpos[p])
+    const uint8_t* qcode;       // query codes (positions qpos[p]; the reverse pass reads rows n-1 .. 0)
     const uint8_t* rcode;       // reference codes (padded positions rpos[p])
     const int64_t* qpos;        // query code position per pair
     const int64_t* rpos;        // reference code position per pair
@@ -83,6 +82,7 @@ struct WaveParams {
     int64_t scratch_seg_bytes;  // bytes of one segment x parity buffer
     unsigned long long* swept;  // cells swept (statistics)
     uint32_t tag_mul;           // = 64; a kernel parameter so the row tag is an IMAD (FMA pipe), not a LEA
+    uint32_t one;               // = 1; a kernel parameter so H = Hb + o is an IMAD (FMA pipe), not an IADD3
     Scoring sc;
 };
 
@@ -193,7 +193,7 @@ __device__ __forceinline__ uint4 lds_rem(uint32_t addr) {
 // references differ by at most the pad margin (the columns past a shorter
 // reference are pad codes, whose cells stay below S).
 template <class T, int W, int K, bool REV, bool MULTI, bool EV, bool TAG>
-__device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const uint32_t sv_base,
+__device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const uint32_t sv_base,
                                       const int seg, const int L, const int s_m, const int (&h_pid)[T::NH],
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
                                       const int mmax, const int row0, const uint32_t o2, const uint32_t e2, const int o,
@@ -205,10 +205,12 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     constexpr int CS = W * G::PB;        // profile bytes per code
     const int nc = P.sc.nc;
 
-    Quads<K> HO;   // H + o of the lane's rows at the previous column
-    uint32_t E[K]; // E of the lane's rows at the previous column
+    Quads<K> HO;   // H of the lane's rows at the previous column (plain, >= 0)
+    uint32_t E[K]; // Eb = E - o of the lane's rows at the previous column (>= 0)
 #pragma unroll
-    for (int r = 0; r < K; ++r) { HO[r] = o2; E[r] = o2; }
+    for (int r = 0; r < K; ++r) { HO[r] = 0u; E[r] = 0u; }
+    const uint32_t floor2 = T::splat(-o);  // Hb floor: H >= 0  <=>  Hb >= -o
+    const uint32_t one = P.one;
     // TAG: the running max holds H*64 + (3 - u)*16 + (15 - r) for the cell of row r in the
     // u-th column of the current 4-column block, so the max itself names the first column of
     // the block and the smallest row holding it (reading R5).  Bookkeeping happens once per
@@ -233,7 +235,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
         ev[h] = (EV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
         next_ev = min(next_ev, ev[h]);
     }
-    uint32_t hoLast = o2, fLast = o2, prevUpHO = o2;
+    uint32_t hoLast = 0u, fLast = 0u, prevUpHO = 0u;
     uint32_t prof_h[NH];  // shared-window address of this lane's profile entries, code 0
     const uint8_t* rp[NH];
 #pragma unroll
@@ -244,12 +246,13 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     const uint32_t cs = opaque(CS);  // code stride as a runtime value: the address is one IMAD
     // lane 0 takes the row above from the stripe boundary: up = shfl * notL0 + b (IMAD)
     const uint32_t notL0 = opaque(L != 0 ? 1u : 0u);
-    const uint32_t b0 = (L == 0) ? o2 : 0u;
+    // (H = 0, F = o above row 0: H = 0, Fb = 0)
+    const uint32_t b0 = 0u;
 
     auto emit = [&](int h) {  // forward result of half h for this lane and stripe
         const int b = TAG ? (T::get(best, h) >> 6) : T::get(best, h);
         if (h_pid[h] >= 0 && b > 0) {
-            const int rr = TAG ? brow[h] : sv_first_row<T, K>(sv[h], h, b + o);
+            const int rr = TAG ? brow[h] : sv_first_row<T, K>(sv[h], h, b);
             atomicMax(P.keys + h_pid[h], pack_key(b, bc[h], row0 + L * K + rr));
         }
     };
@@ -262,10 +265,6 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 const int v = T::get(nbt, h);
                 bc[h] = t0 + (U - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
                 brow[h] = ((1 << RB) - 1) - (v & ((1 << RB) - 1));
-                if (REV && h_pid[h] >= 0 && (v >> 6) == h_tgt[h]) {
-                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], bc[h], row0 + L * K + brow[h]));
-                    atomicMin((int*)stop + seg * NH + h, bc[h] + W);
-                }
             }
         }
         best = nbt | TAGSET;
@@ -283,11 +282,34 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
         if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
     }
 
-    // reverse pass: packed targets of both halves (the forward score S of each pair)
-    uint32_t tgt2 = 0;
+    // reverse pass: packed targets of both halves (the forward score S of each pair); the
+    // TAG route compares block maxima against S*64 (0x7fff: half finished or empty)
+    uint32_t tgt2 = 0, tgt64 = 0;
 #pragma unroll
-    for (int h = 0; h < NH; ++h) tgt2 = T::set(tgt2, h, h_pid[h] >= 0 ? h_tgt[h] : -1);
+    for (int h = 0; h < NH; ++h) {
+        tgt2 = T::set(tgt2, h, h_pid[h] >= 0 ? h_tgt[h] : -1);
+        if (TAG && REV) tgt64 = T::set(tgt64, h, h_pid[h] >= 0 ? h_tgt[h] * 64 : 0x7fff);
+    }
     int found_blk = 0;
+    // TAG reverse pass: some half's block maximum reached S*64.  Every cell of the reversed
+    // rectangle has H <= S, so the block's first cell holding S is named by the tag (reading R6);
+    // a maximum above S can only come from the code bytes past the rectangle (past the pad run
+    // finish_fwd writes after the reversed prefix), i.e. after the half's true first S column.
+    auto rev_tag_find = [&](uint32_t nbt_, int t0) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            const int v = T::get(nbt_, h);
+            if (v >= T::get(tgt64, h)) {
+                const int col = t0 + (U - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
+                if ((v >> 6) == h_tgt[h] && col < h_m[h]) {
+                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], col, row0 + L * K + ((1 << RB) - 1) - (v & ((1 << RB) - 1))));
+                    atomicMin((int*)stop + seg * NH + h, col + W);
+                }
+                tgt64 = T::set(tgt64, h, 0x7fff);
+                found_blk = 1;
+            }
+        }
+    };
     int T_end = mmax + W - 1;
     if (REV) {
         int te = 0;
@@ -298,11 +320,12 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
     // NB blocks of U columns per loop iteration (the longer body lets ptxas keep loop-carried
     // values in place); tag bookkeeping stays per U-column block
     constexpr int NB = REV ? 1 : SW_BODY_BLOCKS;
-    for (int t00 = 0; t00 < T_end; t00 += U * NB) {
+    int t00 = 0;
+    for (; t00 < T_end; t00 += U * NB) {
 #pragma unroll
       for (int bb = 0; bb < NB; ++bb) {
         const int t0 = t00 + bb * U;
-        uint32_t nbt = best;  // TAG: running max of this block
+        uint32_t nbt = REV ? 0u : best;  // TAG: running max of this block
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = t0 + u;
@@ -350,26 +373,15 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 } else {
                     sc = pw[0][r];
                 }
-                E[r] = T::addmax(E[r], e2, HO[r]);          // E[i][j] = max(E[i][j-1] + e, H[i][j-1] + o)
-                F = T::addmax(F, e2, hu);                   // F[i][j] = max(F[i-1][j] + e, H[i-1][j] + o)
-#if SW_CELL_V3
-                // the serial chain per row is F -> H -> HO; X = max(H[i-1][j-1] + s, E, 0)
-                // depends only on the previous column and can issue while the shuffle is in flight
-                const uint32_t x = T::addmax_relu(hd, sc, E[r]);
-                const uint32_t h = T::max2(x, F);            // F may be negative, x >= 0
-#elif SW_CELL_V2
-                // 3-op dependency chain per row (F -> H -> HO): the diagonal term is off the chain
-                const uint32_t x = T::add(hd, sc);          // H[i-1][j-1] + s
-                const uint32_t h = T::max3(x, E[r], F);     // max(., E, F, 0)
-#else
-                const uint32_t tt = T::max_relu(E[r], F);   // max(E, F, 0)
-                const uint32_t h = T::addmax(hd, sc, tt);   // max(H[i-1][j-1] + s, E, F, 0)
-#endif
+                E[r] = T::addmax(E[r], e2, HO[r]);          // Eb[i][j] = max(Eb[i][j-1] + e, H[i][j-1])
+                F = T::addmax(F, e2, hu);                   // Fb[i][j] = max(Fb[i-1][j] + e, H[i-1][j])
+                const uint32_t tt = T::max3(E[r], F, floor2);  // max(E, F, 0) - o
+                const uint32_t hb = T::addmax(hd, sc, tt);  // max(H[i-1][j-1] + s, E, F, 0) - o
                 hd = HO[r];
-                HO[r] = T::add(h, o2);
+                HO[r] = hb * one + o2;                      // H = Hb + o: one IMAD, no borrow (Hb >= -o)
                 hu = HO[r];
                 // TAG: H*64 + tag per half, one IMAD on the FMA pipe (H <= 511: no carry)
-                H[r] = TAG ? h * P.tag_mul + (uint32_t)((U - 1 - u) * (1 << RB) + (1 << RB) - 1 - r) * 0x10001u : h;
+                H[r] = TAG ? HO[r] * P.tag_mul + (uint32_t)((U - 1 - u) * (1 << RB) + (1 << RB) - 1 - r) * 0x10001u : HO[r];
             }
             hoLast = HO[K - 1];
             fLast = F;
@@ -434,7 +446,11 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
                 if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
             }
         }
-        if (TAG && nbt != best) tag_commit(nbt, t0);
+        if (TAG && !REV && nbt != best) tag_commit(nbt, t0);
+        if (TAG && REV) {
+            const uint32_t x = T::max2(nbt, tgt64) ^ nbt;  // zero half: block max >= S*64
+            if (((x - 0x00010001u) & ~x & 0x80008000u) != 0u) rev_tag_find(nbt, t0);
+        }
         if (REV && __any_sync(FULL, found_blk)) {  // re-read the stop columns only after a find
             __syncwarp();
             int te = 0;
@@ -449,6 +465,7 @@ __device__ __forceinline__ void sweep(const WaveParams& P, const uint8_t* prof, 
 #pragma unroll
         for (int h = 0; h < NH; ++h) emit(h);
     }
+    return t00;  // column steps swept (statistics)
 }
 
 template <class T, int W, int K, bool REV, bool TAG>
@@ -456,10 +473,10 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
-    // Row/column tags are used only in forward sweeps without end events: there every
-    // computed cell past a reference is a pad cell (H < S <= 511), so H*64 cannot carry
-    // into the other half.  Event items and the reverse pass use the plain s16 logic.
-    constexpr bool TAGF = TAG && !REV;
+    // Row/column tags (H*64 + tag) need H <= 511 in every computed cell, also past a half's
+    // reference: forward items without end events (the columns past a reference are pad
+    // codes) and reverse items with max_s * rows <= 511 (finish_fwd routes the rest to S16).
+    constexpr bool TAGF = TAG;
     extern __shared__ __align__(16) uint8_t smem[];
     // substitution table for the profile builds, in shared memory: lanes index it with
     // divergent codes, which a constant-bank table would serialise
@@ -488,7 +505,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
     int first = 0;
     for (int r = 0; r < P.route; ++r) first += P.counts[r];
     const int items = (n_path + SLOTS - 1) / SLOTS;
-    const uint32_t o2 = T::splat(P.sc.gap_open);
+    const uint32_t o2 = T::lift(P.sc.gap_open);  // H = Hb + o as one 32-bit add
     const uint32_t e2 = T::splat(P.sc.gap_extend);
     const int o = P.sc.gap_open;
 
@@ -536,8 +553,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
             h_rpos[h] = __shfl_sync(FULL, s_rpos, sl);
             if (h_pid[h] < 0) h_rpos[h] = PADL;  // empty slot: read pad region at buffer start
         }
-        const int T_steps = mmax + W - 1;
-        if (lane == 0) atomicAdd(P.swept, (unsigned long long)ns * G::ROWS * (unsigned long long)T_steps * SLOTS);
+        unsigned long long steps = 0;  // column steps over the item's stripes
 
         if (REV) {
             __syncwarp();
@@ -558,13 +574,35 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
                     const int l = (cb / G::PWORDS) % W;
                     const int w = cb % G::PWORDS;
                     uint8_t* base = prof + (size_t)sl * nc * W * G::PB + (size_t)l * G::PB + w * 4;
-                    if (NH == 2) {
+                    if (NH == 2 && P.sc.alphabet == SW_ALPHABET_DNA) {
+                        // DNA: s(q, c) is match / mismatch, four rows per word with byte-SIMD
+                        uint32_t q4 = 0u, inv = 0u;  // query codes; 0xff bytes for rows without a residue
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int r = w * 4 + b;
+                            const int i = row0 + l * K + r;
+                            if (pid >= 0 && r < K && i < n) q4 |= (uint32_t)P.qcode[REV ? qp + n - 1 - i : qp + i] << (8 * b);
+                            else inv |= 0xffu << (8 * b);
+                        }
+                        const uint32_t mi = (uint32_t)((P.sc.mismatch - o) & 0xff) * 0x01010101u;
+                        const uint32_t dm = ((uint32_t)((P.sc.match - o) & 0xff) * 0x01010101u) ^ mi;
+                        const uint32_t padw = 0x80808080u;  // -128 per byte
+                        for (int c = 0; c < nc - 1; ++c) {
+                            const uint32_t x = q4 ^ ((uint32_t)c * 0x01010101u);
+                            // 0x80 in every byte of x that is zero (exact: no carries across bytes)
+                            const uint32_t z = ~(((x & 0x7f7f7f7fu) + 0x7f7f7f7fu) | x | 0x7f7f7f7fu);
+                            const uint32_t eq = (z >> 7) * 0xffu;
+                            const uint32_t word = (((eq & dm) ^ mi) & ~inv) | (inv & padw);
+                            *reinterpret_cast<uint32_t*>(base + (size_t)c * W * G::PB) = word;
+                        }
+                        *reinterpret_cast<uint32_t*>(base + (size_t)(nc - 1) * W * G::PB) = padw;
+                    } else if (NH == 2) {
                         int qc[4];
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const int r = w * 4 + b;
                             const int i = row0 + l * K + r;
-                            qc[b] = (pid >= 0 && r < K && i < n) ? P.qcode[qp + i] : -1;
+                            qc[b] = (pid >= 0 && r < K && i < n) ? P.qcode[REV ? qp + n - 1 - i : qp + i] : -1;
                         }
                         for (int c = 0; c < nc; ++c) {
                             uint32_t word = 0;
@@ -579,7 +617,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
                     } else {
                         const int r = w;
                         const int i = row0 + l * K + r;
-                        const int qc = (pid >= 0 && r < K && i < n) ? P.qcode[qp + i] : -1;
+                        const int qc = (pid >= 0 && r < K && i < n) ? P.qcode[REV ? qp + n - 1 - i : qp + i] : -1;
                         for (int c = 0; c < nc; ++c) {
                             int v = -(1 << 29);
                             if (qc >= 0 && c < nc - 1) v = sigma(qc, c) - o;
@@ -593,10 +631,10 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
             // ---- the stripe's column sweep (single-stripe items skip all hand-off code) ----
             if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
-                    sweep<T, W, K, REV, false, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
                 else
-                    sweep<T, W, K, REV, false, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                       row0, o2, e2, o, nullptr, nullptr, false, false);
             } else {
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
@@ -604,13 +642,14 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
                 uint2* scr_out = reinterpret_cast<uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
                 if (need_ev)
-                    sweep<T, W, K, REV, true, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
                 else
-                    sweep<T, W, K, REV, true, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
             }
         }
+        if (lane == 0) atomicAdd(P.swept, steps * G::ROWS * SLOTS);
     }
 }
 

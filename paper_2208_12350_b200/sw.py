@@ -32,7 +32,7 @@ SW_STAGE_NAMES = ("pack", "sort", "fwd", "mid", "rev", "finish")
 
 EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
-            "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_dpx_peak")
+            "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_last_reverse_cells", "sw_dpx_peak")
 
 
 class sw_scoring_t(ctypes.Structure):
@@ -87,6 +87,7 @@ def load(build_if_missing: bool = True):
     lib.sw_get_stage_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_float)]
     lib.sw_last_launch_count.argtypes = [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.sw_last_cell_counts.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.sw_last_reverse_cells.argtypes = [vp, ctypes.POINTER(i64)]
     lib.sw_dpx_peak.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double), vp]
     for name in EXPORTED:
         if name not in ("sw_status_string", "sw_last_error_message"):
@@ -253,6 +254,11 @@ class Aligner:
         a, b = ctypes.c_int32(0), ctypes.c_int32(0)
         load().sw_last_launch_count(ctypes.c_void_p(self.handle), ctypes.byref(a), ctypes.byref(b))
         return a.value, b.value
+
+    def reverse_cells(self):
+        a = ctypes.c_int64(0)
+        load().sw_last_reverse_cells(ctypes.c_void_p(self.handle), ctypes.byref(a))
+        return a.value
 
     def cell_counts(self):
         a, b = ctypes.c_int64(0), ctypes.c_int64(0)

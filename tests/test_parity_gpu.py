@@ -167,6 +167,34 @@ def test_stripe_and_lane_boundaries(aligner):
     run_and_compare(aligner, synth.from_pairs(pairs, synth.DNA_SCORING))
 
 
+def test_pack_vector_edges_and_bad_symbol_attribution(aligner):
+    """Tiny and ragged sequences packed 32 pairs per warp (16-byte vectors straddling pairs,
+    pads and warp spans), bad symbols at the start / middle / end of one pair among valid
+    neighbours, and reversed prefixes ending at every column phase."""
+    rng = np.random.default_rng(21)
+    lens = (0, 1, 2, 3, 7, 15, 16, 17, 31, 32, 33, 47, 64, 65, 100)
+    pairs = []
+    for k in range(200):
+        n = int(lens[k % len(lens)]); m = int(lens[(k * 7 + 3) % len(lens)])
+        q = "".join(rng.choice(list("ACGT"), n)); r = "".join(rng.choice(list("ACGT"), m))
+        if k % 23 == 5 and n:
+            pos = (0, n // 2, n - 1)[k % 3]
+            q = q[:pos] + "X" + q[pos + 1:]
+        if k % 29 == 7 and m:
+            pos = (0, m // 2, m - 1)[k % 3]
+            r = r[:pos] + "#" + r[pos + 1:]
+        pairs.append((q, r))
+    # identical pairs: the alignment ends at every column phase 0..15 of the reference
+    for m in range(20, 52):
+        r = "".join(rng.choice(list("ACGT"), m))
+        pairs.append((r[m - 18:m - 2], r))
+    run_and_compare(aligner, synth.from_pairs(pairs, synth.DNA_SCORING))
+    prot = [("".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), int(lens[k % 15]))),
+             "".join(rng.choice(list("ACDEFGHIKLMNPQRSTVWY"), int(lens[(k * 5 + 1) % 15])))) for k in range(120)]
+    prot[17] = (prot[17][0] + "J", prot[17][1])
+    run_and_compare(aligner, synth.from_pairs(prot, synth.PROTEIN_SCORING))
+
+
 def test_int32_routing_per_pair(aligner):
     """s16-eligible scoring, but pairs whose max score exceeds the int16 bound go to the s32 kernel."""
     sc = {"alphabet": "dna", "match": 30, "mismatch": -20, "gap_open": -40, "gap_extend": -5}
@@ -179,6 +207,26 @@ def test_int32_routing_per_pair(aligner):
         pairs.append(("".join(rng.choice(list("ACGT"), 60)), "".join(rng.choice(list("ACGT"), 90))))
     got = run_and_compare(aligner, synth.from_pairs(pairs, sc))
     assert got["score"][0] > 32767
+
+
+def test_three_routes_in_one_counting_sorted_batch(aligner):
+    """TAG (max score <= 511), S16 and S32 pairs in one batch whose work keys all fit the exact
+    counting-sort bins (references < 1,040, <= 8 stripes): route groups and their offsets in the
+    pair order must line up for both passes."""
+    sc = {"alphabet": "dna", "match": 100, "mismatch": -20, "gap_open": -25, "gap_extend": -5}
+    rng = np.random.default_rng(31)
+    pairs = []
+    for k in range(300):
+        n = int(rng.integers(1, 700)) if k % 3 else int(rng.integers(1, 6))
+        m = int(rng.integers(1, 1000)) if k % 3 else int(rng.integers(1, 6))
+        q = "".join(rng.choice(list("ACGT"), n))
+        if k % 2 and n > 20 and m > n:
+            r = "".join(rng.choice(list("ACGT"), m - n)) + q
+        else:
+            r = "".join(rng.choice(list("ACGT"), m))
+        pairs.append((q, r))
+    got = run_and_compare(aligner, synth.from_pairs(pairs, sc))
+    assert got["score"].max() > 32000 and (got["score"][::3] <= 511).all()
 
 
 def test_int32_routing_whole_scoring(aligner):

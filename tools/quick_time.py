@@ -38,5 +38,8 @@ print(f"{cfg}: median {ms:.3f} ms  -> {cells/ms/1e6:.1f} GCUPS (whole call)")
 st = {k: float(np.median([x[k] for x in stages])) for k in stages[0]}
 print("stages ms:", {k: round(v, 4) for k, v in st.items()})
 print(f"fwd kernel GCUPS = {cells/st['fwd']/1e6:.1f}; swept/real = {swept/max(fwd,1):.3f}")
+rsw = a.reverse_cells()
+print(f"rev swept cells = {rsw:.4g} ({rsw/max(fwd,1):.3f} of fwd real); rev kernel swept GCUPS = {rsw/st['rev']/1e6:.1f}; "
+      f"fwd kernel swept GCUPS = {swept/st['fwd']/1e6:.1f}")
 print("launches:", a.launch_count(), "status:", a.batch_status())
 print("dpx peak TCUPS:", sw.sw_dpx_peak(0, 200.0) / 1e12)
