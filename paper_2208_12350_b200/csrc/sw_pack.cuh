@@ -57,11 +57,12 @@ struct PackParams {
 __device__ __forceinline__ uint8_t ascii_code(int alphabet, int ch) {
     if (ch >= 'a' && ch <= 'z') ch -= 32;
     if (alphabet == SW_ALPHABET_DNA) {
+        // A0 C1 T2 G3: bits 2:1 of the letter (dna4 below computes the same codes four at a time)
         switch (ch) {
             case 'A': return 0;
             case 'C': return 1;
-            case 'G': return 2;
-            case 'T': return 3;
+            case 'T': return 2;
+            case 'G': return 3;
             default: return CODE_BAD;
         }
     }
@@ -83,25 +84,46 @@ __device__ __forceinline__ uint32_t conv4(uint32_t w, const uint8_t* lut, uint32
     return c0 | (c1 << 8) | (c2 << 16) | (c3 << 24);
 }
 
+// DNA, four ASCII bytes at a time: code = bits 2:1 of the upper-cased letter (A0 C1 T2 G3);
+// a byte is valid iff the letter of its code equals it (one PRMT table lookup).  *nz gets
+// 0x80 in every invalid byte.
+__device__ __forceinline__ uint32_t dna4(uint32_t w, uint32_t& nz) {
+    const uint32_t u = w & 0xdfdfdfdfu;
+    const uint32_t c = (u >> 1) & 0x03030303u;
+    const uint32_t t = c | (c >> 4);                      // bytes 0 / 2: two codes as nibbles
+    const uint32_t sel = __byte_perm(t, 0u, 0x4420u);     // four 2-bit selectors
+    const uint32_t diff = __byte_perm(0x47544341u, 0u, sel) ^ u;  // 'A' 'C' 'T' 'G'
+    nz = (((diff & 0x7f7f7f7fu) + 0x7f7f7f7fu) | diff) & 0x80808080u;
+    return c;
+}
+
+// Codes of 16 ASCII bytes (DNA: arithmetic, protein: table) and their invalid-byte
+// markers (0x80 per invalid byte).
+__device__ __forceinline__ void conv16m(const uint4 v, bool dna, const uint8_t* lut, uint32_t (&c)[4], uint32_t (&nz)[4]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (dna) {
+            c[q] = dna4(w[q], nz[q]);
+        } else {
+            uint32_t bm = 0;
+            c[q] = conv4(w[q], lut, bm);
+            nz[q] = c[q] & 0x80808080u;  // CODE_BAD = 0xff, valid codes < 25
+        }
+    }
+}
+
+// Byte mask of word q from a 16-bit per-byte mask.
+__device__ __forceinline__ uint32_t expand_nibble(uint32_t m16, int q) {
+    const uint32_t nib = (m16 >> (4 * q)) & 0xfu;
+    return ((nib * 0x00204081u) & 0x01010101u) * 0xffu;
+}
+
 // Byte-wise conversion of one code position (partial vectors at span edges).
 __device__ __forceinline__ uint8_t conv1(uint8_t ch, const uint8_t* lut, uint8_t bad_to, bool& bad) {
     const uint8_t c = lut[ch];
     if (c == CODE_BAD) { bad = true; return bad_to; }
     return c;
-}
-
-// 16 bytes -> codes; CODE_BAD (0xff) bytes stay 0xff (bit 7 marks them: valid codes are < 25).
-__device__ __forceinline__ uint4 conv16_raw(uint4 v, const uint8_t* lut) {
-    uint32_t bm = 0;
-    return make_uint4(conv4(v.x, lut, bm), conv4(v.y, lut, bm), conv4(v.z, lut, bm), conv4(v.w, lut, bm));
-}
-
-// Byte mask of bytes [lo, hi) (0 <= lo <= hi <= 16) within 32-bit word q of a 16-byte vector.
-__device__ __forceinline__ uint32_t byte_range_mask(int lo, int hi, int q) {
-    const int a = min(max(lo - 4 * q, 0), 4), b = min(max(hi - 4 * q, 0), 4);
-    const uint32_t mb = b >= 4 ? 0xffffffffu : ((1u << (8 * b)) - 1u);
-    const uint32_t ma = a >= 4 ? 0xffffffffu : ((1u << (8 * a)) - 1u);
-    return mb & ~ma;
 }
 
 // Largest k in [0, cnt) with a[k] <= x (a non-decreasing; k = 0 if none).
@@ -161,6 +183,7 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const uint8_t pad_code = (uint8_t)((P.alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN) - 1);
     const uint32_t padw = (uint32_t)pad_code * 0x01010101u;
+    const bool dna = P.alphabet == SW_ALPHABET_DNA;
     int l_bad = 0, l_route[N_ROUTES] = {0, 0, 0}, l_maxn = 0, l_maxm = 0, l_malf = 0;
     unsigned long long l_cells = 0;
     int64_t* slot = s_slot[wib];
@@ -217,30 +240,20 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
                     if (vb + u * 32 + lane > v_hi) continue;
                     const int64_t y0 = (vb + u * 32 + lane) * 16;
                     uint4 o = make_uint4(padw, padw, padw, padw);
-                    if (rs[u] == 0 && re[u] == 16) {  // common case: the whole vector is reference bytes
-                        uint32_t bm = 0;
-                        o = make_uint4(conv4(src[u].x, lut, bm), conv4(src[u].y, lut, bm), conv4(src[u].z, lut, bm),
-                                       conv4(src[u].w, lut, bm));
-                        if (bm & 0x80u) {
-                            badbits |= 1u << kk[u];
-                            auto fix = [&](uint32_t w) {
-                                const uint32_t bb = ((w & 0x80808080u) >> 7) * 0xffu;
-                                return (w & ~bb) | (padw & bb);
-                            };
-                            o = make_uint4(fix(o.x), fix(o.y), fix(o.z), fix(o.w));
-                        }
-                    } else if (re[u] > rs[u]) {
-                        const uint4 c = conv16_raw(src[u], lut);
-                        const uint32_t cw[4] = {c.x, c.y, c.z, c.w};
-                        uint32_t ow[4];
-                        uint32_t badacc = 0;
+                    if (re[u] > rs[u]) {
+                        // reference bytes [rs, re) of the vector converted, the rest (and invalid
+                        // symbols) pad codes
+                        uint32_t c[4], nz[4];
+                        conv16m(src[u], dna, lut, c, nz);
+                        const uint32_t r16 = ((1u << re[u]) - 1u) ^ ((1u << rs[u]) - 1u);
+                        uint32_t ow[4], badacc = 0;
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const uint32_t rm = byte_range_mask(rs[u], re[u], q);
-                            const uint32_t bb = ((cw[q] & 0x80808080u) >> 7) * 0xffu & rm;  // bad bytes of the reference
+                            const uint32_t rm = expand_nibble(r16, q);
+                            const uint32_t bb = ((nz[q] >> 7) * 0xffu) & rm;
                             badacc |= bb;
                             const uint32_t keep = rm & ~bb;
-                            ow[q] = (cw[q] & keep) | (padw & ~keep);
+                            ow[q] = (c[q] & keep) | (padw & ~keep);
                         }
                         if (badacc) badbits |= 1u << kk[u];
                         o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
@@ -274,19 +287,19 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
                     for (int u = 0; u < PACK_FB; ++u) {
                         if (vb + u * 32 + lane > qv_hi) continue;
                         const int64_t y0 = (vb + u * 32 + lane) * 16;
-                        uint32_t bm = 0;
-                        uint32_t cw[4] = {conv4(src[u].x, lut, bm), conv4(src[u].y, lut, bm), conv4(src[u].z, lut, bm),
-                                          conv4(src[u].w, lut, bm)};
-                        if (bm & 0x80u) {
+                        uint32_t cw[4], nz[4];
+                        conv16m(src[u], dna, lut, cw, nz);
+                        if ((nz[0] | nz[1] | nz[2] | nz[3]) != 0u) {
                         const int lo16 = qlo - y0 > 0 ? (int)(qlo - y0) : 0, hi16 = qhi - y0 < 16 ? (int)(qhi - y0) : 16;
+                        const uint32_t r16 = ((1u << hi16) - 1u) ^ ((1u << lo16) - 1u);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
-                            const uint32_t bb = ((cw[q] & 0x80808080u) >> 7) * 0xffu & byte_range_mask(lo16, hi16, q);
+                            const uint32_t bb = ((nz[q] >> 7) * 0xffu) & expand_nibble(r16, q);
                             if (bb) {  // rare: attribute each bad byte to its pair, store pads instead
                                 for (int b = 0; b < 4; ++b)
                                     if ((bb >> (8 * b)) & 0xffu) badbits |= 1u << owner_of(sqa, cnt, y0 + qd + 4 * q + b);
-                                cw[q] = (cw[q] & ~bb) | (padw & bb);
                             }
+                            cw[q] = (cw[q] & ~bb) | (padw & bb);
                         }
                         }
                         store16_within(P.qcode, y0, make_uint4(cw[0], cw[1], cw[2], cw[3]), qlo, qhi);
