@@ -126,6 +126,30 @@ sw_status_t sw_align_batch_host(sw_handle_t h,
                                 int64_t n_pairs, const sw_scoring_t* scoring,
                                 const sw_result_t* out_host, void* stream);
 
+/*
+ * Asynchronous HOST-buffer entry point for a stream of batches (the serving
+ * loop): enqueues this batch's host->device copies on a handle-owned copy
+ * stream, the alignment on `stream`, and the device->host result copies on a
+ * second handle-owned copy stream, and returns without waiting.  Two batches
+ * can be in flight: while batch i is aligned on `stream`, batch i+1's inputs
+ * are copied in (double-buffered staging), so a stream of batches runs at the
+ * alignment's rate rather than alignment + transfer.  Batches are aligned in
+ * submission order.  The caller keeps every host buffer of a submitted batch
+ * (inputs and out_host) untouched until sw_wait returns.  Arguments as for
+ * sw_align_batch_host (q_offsets / r_offsets are read on the host during the
+ * call: validation and work estimates); the same validation errors are
+ * returned synchronously, before anything is enqueued.
+ */
+sw_status_t sw_submit_host(sw_handle_t h,
+                           const uint8_t* queries, const int64_t* q_offsets,
+                           const uint8_t* refs, const int64_t* r_offsets,
+                           int64_t n_pairs, const sw_scoring_t* scoring,
+                           const sw_result_t* out_host, void* stream);
+
+/* Wait until every batch submitted with sw_submit_host is on the host and make
+ * `stream` (the one passed to sw_submit_host) wait for it too. */
+sw_status_t sw_wait(sw_handle_t h);
+
 /* Synchronise the handle's last batch and report how many pairs were
  * invalid.  Returns SW_OK, SW_ERR_BAD_PAIRS (count > 0) or SW_ERR_INTERNAL. */
 sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs);

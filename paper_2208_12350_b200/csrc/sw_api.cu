@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -47,7 +48,8 @@ struct DevBuf {
 
 }  // namespace
 
-constexpr int MAX_CHUNKS = 4;
+constexpr int MAX_CHUNKS = 8;
+constexpr int N_SLOTS = 2;
 
 struct sw_context {
     int device = 0;
@@ -66,23 +68,36 @@ struct sw_context {
     DevBuf<unsigned long long> keys_fwd, keys_rev;
     // codes
     DevBuf<uint8_t> qcode, rcode, rrev;
-    // misc
-    DevBuf<uint8_t> scratch, cub_temp;
-    BatchStats* d_stats = nullptr;
-    BatchStats* h_stats = nullptr;
+    // misc.  Per-slot state: the host-buffer entry point runs consecutive chunks of one batch
+    // on two streams (slot k & 1), so their small kernels and tails overlap; slot 0 is the
+    // device entry point's.
+    DevBuf<uint8_t> scratch[N_SLOTS], cub_temp[N_SLOTS];
+    BatchStats* d_stats = nullptr;  // [N_SLOTS]
+    BatchStats* h_stats = nullptr;  // [N_SLOTS] (pinned)
     int64_t* h_ext = nullptr;
-    int32_t* d_counters = nullptr;  // work-queue heads: 3 forward + 3 reverse routes
+    int32_t* d_counters = nullptr;  // [N_SLOTS][8] work-queue heads: 3 forward + 3 reverse routes
     uint32_t* d_sink = nullptr;
-    uint32_t* d_hist = nullptr;     // work-bin histogram [NBINS] (kept zero between passes)
-    uint32_t* d_binbase = nullptr;  // bin cursors [NBINS]
+    uint32_t* d_hist = nullptr;     // [N_SLOTS][NBINS] work-bin histogram (kept zero between passes)
+    uint32_t* d_binbase = nullptr;  // [N_SLOTS][NBINS] bin cursors
+    cudaStream_t aux_stream = nullptr;  // slot 1's stream
     // host-buffer entry point staging
     DevBuf<uint8_t> st_q, st_r;
     DevBuf<int64_t> st_qo, st_ro;
     DevBuf<int32_t> st_out;
+    // asynchronous host-buffer entry point: double-buffered staging, copy-in / copy-out streams
+    DevBuf<uint8_t> as_q[2], as_r[2];
+    DevBuf<int64_t> as_qo[2], as_ro[2];
+    DevBuf<int32_t> as_out[2];
+    cudaEvent_t as_in[2] = {}, as_comp[2] = {}, as_done[2] = {}, as_start = nullptr;
+    bool as_used[2] = {false, false};
+    bool as_inflight = false;
+    int as_next = 0;
+    cudaStream_t out_stream = nullptr;   // device -> host result copies
+    cudaStream_t as_stream = nullptr;    // the caller's stream of the submitted batches
 
     int codes_alphabet = -1;  // alphabet the code buffers were last cleared for
     cudaStream_t copy_stream = nullptr;  // host-buffer entry point: overlapped copies
-    cudaEvent_t ev_in[8] = {}, ev_out[8] = {};
+    cudaEvent_t ev_in[MAX_CHUNKS] = {}, ev_out[MAX_CHUNKS] = {}, ev_prep = nullptr;
     bool timing = false;
     cudaEvent_t ev[8] = {};
     bool ev_valid = false;
@@ -199,40 +214,82 @@ Launch plan_wave(const sw_context* h, const void* kernel, int nc, int64_t n_path
 // What the host already knows about a batch (host-buffer entry point): with it the
 // pipeline needs no stream synchronisation between enqueueing and completion.
 struct HostPlan {
-    int64_t ext[4];            // q0, qN, r0, rN
-    int32_t max_n, max_m;      // longest query / reference of the batch
+    int64_t ext[4];            // q0, qN, r0, rN of the whole batch (code positions are batch-global)
+    int64_t lo, hi;            // this chunk's pairs
+    int32_t max_n, max_m;      // longest query / reference of the chunk
     int32_t route_upper[N_ROUTES];  // pairs per route by lengths alone (>= the device's counts)
-    bool reset_cumulative;     // first chunk of a user call
+    bool reset_cumulative;     // first chunk of the slot in a user call
+    int slot;                  // per-slot state (statistics, queues, bins, scratch)
 };
+
+// Workspace for a batch of N pairs with tq / tr payload bytes (every chunk of a host-buffer
+// call uses the batch's sizes, so no buffer moves while two streams run).
+sw_status_t prepare_workspace(sw_context* h, size_t N, size_t tq, size_t tr, int alphabet, cudaStream_t s) {
+#define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
+    ENS(nlen, N); ENS(mlen, N); ENS(nlen_rev, N); ENS(mlen_rev, N); ENS(target, N); ENS(iota, N);
+    ENS(order, N); ENS(order_rev, N); ENS(qpos, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
+    ENS(keys_fwd, N); ENS(keys_rev, N);
+    ENS(qcode, tq + 32);
+    // Every byte of the reference code buffers must be a valid code of the batch's
+    // alphabet: finished halves of a work item keep reading past their reference.
+    const size_t rbytes = tr + N * (PADL + PADR) + GUARD + 16;
+    uint8_t* old_r = h->rcode.p; uint8_t* old_rr = h->rrev.p;
+    ENS(rcode, rbytes); ENS(rrev, rbytes);
+    if (h->rcode.p != old_r || h->rrev.p != old_rr || h->codes_alphabet != alphabet) {
+        SW_CUDA(h, cudaMemsetAsync(h->rcode.p, 0, h->rcode.cap, s));
+        SW_CUDA(h, cudaMemsetAsync(h->rrev.p, 0, h->rrev.cap, s));
+        h->codes_alphabet = alphabet;
+    }
+#undef ENS
+    return SW_OK;
+}
+
+// Cumulative statistics of the last user call: slot 0's, plus slot 1's totals.
+cudaError_t read_stats(sw_context* h, BatchStats& t) {
+    cudaError_t e = cudaMemcpy(h->h_stats, h->d_stats, N_SLOTS * sizeof(BatchStats), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return e;
+    t = h->h_stats[0];
+    for (int k = 1; k < N_SLOTS; ++k) {
+        const BatchStats& u = h->h_stats[k];
+        t.n_bad += u.n_bad; t.internal_err += u.internal_err; t.cells += u.cells;
+        t.swept_fwd += u.swept_fwd; t.swept_rev += u.swept_rev; t.malformed |= u.malformed;
+    }
+    return cudaSuccess;
+}
 
 // Order the pairs by work key (h->key), most work first.  Small-region batches
 // (sw_bin.cuh): counting sort on the exact bins pack / finish_fwd histogrammed;
 // otherwise a radix sort of the full 32-bit keys.  Leaves the histogram zero.
-sw_status_t bin_order(sw_context* h, int32_t* order, int64_t n_pairs, bool small, cudaStream_t s) {
+sw_status_t bin_order(sw_context* h, int32_t* order, int64_t lo, int64_t hi, bool small, int slot, cudaStream_t s) {
+    uint32_t* hist = h->d_hist + (size_t)slot * NBINS;
+    uint32_t* base = h->d_binbase + (size_t)slot * NBINS;
+    const int64_t n = hi - lo;
     if (small) {
-        bin_scan_kernel<<<1, BIN_SCAN_THREADS, BIN_SCAN_SMEM, s>>>(h->d_hist, h->d_binbase);
-        const int blocks = (int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 8);
-        bin_scatter_kernel<<<blocks, 256, 0, s>>>(h->key.p, h->d_binbase, order, n_pairs);
+        bin_scan_kernel<<<1, BIN_SCAN_THREADS, BIN_SCAN_SMEM, s>>>(hist, base);
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->sm_count * 8);
+        bin_scatter_kernel<<<blocks, 256, 0, s>>>(h->key.p, base, order, lo, hi);
         SW_CUDA(h, cudaGetLastError());
         h->own_launches += 2;
         return SW_OK;
     }
-    SW_CUDA(h, cudaMemsetAsync(h->d_hist, 0, NBINS * sizeof(uint32_t), s));
+    SW_CUDA(h, cudaMemsetAsync(hist, 0, NBINS * sizeof(uint32_t), s));
     size_t tb = 0;
-    SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p, h->key_sorted.p, h->iota.p, order,
-                                                         (int)n_pairs, 0, 32, s));
+    SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p + lo, h->key_sorted.p + lo, h->iota.p + lo,
+                                                         order, (int)n, 0, 32, s));
     {
-        sw_status_t e = ensure(h, h->cub_temp, tb);
+        sw_status_t e = ensure(h, h->cub_temp[slot], tb);
         if (e != SW_OK) return e;
     }
-    tb = h->cub_temp.cap;
-    SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp.p, tb, h->key.p, h->key_sorted.p, h->iota.p, order,
-                                                         (int)n_pairs, 0, 32, s));
+    tb = h->cub_temp[slot].cap;
+    SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(h->cub_temp[slot].p, tb, h->key.p + lo, h->key_sorted.p + lo,
+                                                         h->iota.p + lo, order, (int)n, 0, 32, s));
     ++h->lib_launches;
     return SW_OK;
 }
 
-// The batch pipeline on device pointers.  host_ext (optional) = {q0, qN, r0, rN}.
+// The batch pipeline on device pointers.  host_ext (optional) = {q0, qN, r0, rN}.  With a
+// HostPlan, only the plan's pairs [lo, hi) of the n_pairs-pair batch are processed, on the
+// plan's slot, with no stream synchronisation.
 sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_off, const uint8_t* refs,
                        const int64_t* r_off, int64_t n_pairs, const sw_scoring_t* scoring,
                        const sw_result_t* out, cudaStream_t s, const int64_t* host_ext,
@@ -246,10 +303,15 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (st != SW_OK) return st;
     if (n_pairs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs < 0");
     if (n_pairs > 0x7ffffff0LL) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs exceeds 2^31 - 16");
-    if (!hp || hp->reset_cumulative) {
+    if (!hp || (hp->reset_cumulative && hp->slot == 0)) {
         h->own_launches = 0;
         h->lib_launches = 0;
     }
+    const int slot = hp ? hp->slot : 0;
+    const int64_t lo = hp ? hp->lo : 0, hi = hp ? hp->hi : n_pairs;
+    BatchStats* stats = h->d_stats + slot;
+    uint32_t* hist = h->d_hist + (size_t)slot * NBINS;
+    int32_t* counters = h->d_counters + slot * 8;
     h->ev_valid = false;
     if (n_pairs == 0) return SW_OK;
     if (!queries || !q_off || !refs || !r_off || !out || !out->score || !out->q_end || !out->r_end ||
@@ -275,58 +337,46 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     const int64_t q0 = ext[0], qN = ext[1], r0 = ext[2], rN = ext[3];
     const size_t N = (size_t)n_pairs;
     if (qN < q0 || rN < r0) {
-        fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, n_pairs);
+        fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, 0, n_pairs);
         return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
     }
     const size_t tq = (size_t)(qN - q0), tr = (size_t)(rN - r0);
-    const size_t rbytes = tr + N * (PADL + PADR) + GUARD + 16;
     // code buffers keep the payloads' 16-byte phase so pack moves aligned vectors
     const int64_t qshift = (int64_t)(((uintptr_t)(queries + q0)) & 15);
     const int64_t rshift = (int64_t)(((uintptr_t)(refs + r0)) & 15);
 
     // 2. workspace
+    st = prepare_workspace(h, N, tq, tr, sc.alphabet, s);
+    if (st != SW_OK) return st;
 #define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
-    ENS(nlen, N); ENS(mlen, N); ENS(nlen_rev, N); ENS(mlen_rev, N); ENS(target, N); ENS(iota, N);
-    ENS(order, N); ENS(order_rev, N); ENS(qpos, N); ENS(rpos, N); ENS(flags, N); ENS(key, N); ENS(key_sorted, N);
-    ENS(keys_fwd, N); ENS(keys_rev, N);
-    ENS(qcode, tq + 32);
-    {
-        // Every byte of the reference code buffers must be a valid code of the batch's
-        // alphabet: finished halves of a work item keep reading past their reference.
-        uint8_t* old_r = h->rcode.p; uint8_t* old_rr = h->rrev.p;
-        ENS(rcode, rbytes); ENS(rrev, rbytes);
-        if (h->rcode.p != old_r || h->rrev.p != old_rr || h->codes_alphabet != sc.alphabet) {
-            SW_CUDA(h, cudaMemsetAsync(h->rcode.p, 0, h->rcode.cap, s));
-            SW_CUDA(h, cudaMemsetAsync(h->rrev.p, 0, h->rrev.cap, s));
-            h->codes_alphabet = sc.alphabet;
-        }
-    }
 
     const bool protein = sc.alphabet == SW_ALPHABET_PROTEIN;
     const int rows16 = protein ? GP::ROWS : G16::ROWS, rows32 = G32::ROWS;
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[0], s));
+    const bool timing = h->timing && !hp;
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[0], s));
 
     // 3. pack
-    if (!hp || hp->reset_cumulative) SW_CUDA(h, cudaMemsetAsync(h->d_stats, 0, sizeof(BatchStats), s));
-    else SW_CUDA(h, cudaMemsetAsync(reinterpret_cast<uint8_t*>(h->d_stats) + STATS_PER_BATCH_OFFSET, 0,
+    if (!hp) SW_CUDA(h, cudaMemsetAsync(h->d_stats, 0, N_SLOTS * sizeof(BatchStats), s));  // all slots' totals
+    else if (hp->reset_cumulative) SW_CUDA(h, cudaMemsetAsync(stats, 0, sizeof(BatchStats), s));
+    else SW_CUDA(h, cudaMemsetAsync(reinterpret_cast<uint8_t*>(stats) + STATS_PER_BATCH_OFFSET, 0,
                                     sizeof(BatchStats) - STATS_PER_BATCH_OFFSET, s));
     {
         PackParams P;
-        P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.n_pairs = n_pairs;
+        P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.lo = lo; P.hi = hi;
         P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
         P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA) ? 1 : 0;  // TAG route: DNA batches
         P.rows_s16 = rows16; P.rows_s32 = rows32;
         P.qcode = h->qcode.p; P.rcode = h->rcode.p;
         P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
-        P.hist = h->d_hist; P.keys_fwd = h->keys_fwd.p; P.iota = h->iota.p; P.stats = h->d_stats;
-        // one warp per 32 pairs, at most one full wave of warps
-        const int64_t warps = std::min<int64_t>((n_pairs + 31) / 32, (int64_t)h->sm_count * 64);
+        P.hist = hist; P.keys_fwd = h->keys_fwd.p; P.iota = h->iota.p; P.stats = stats;
+        // one warp per PACK_PPW pairs, at most one full wave of warps
+        const int64_t warps = std::min<int64_t>((hi - lo + PACK_PPW - 1) / PACK_PPW, (int64_t)h->sm_count * 64);
         const int blocks = (int)((warps + PACK_WARPS - 1) / PACK_WARPS);
         pack_kernel<<<blocks, PACK_WARPS * 32, 0, s>>>(P);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
     }
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
     // 4. statistics -> grids and scratch (read back, unless the host already knows bounds)
     BatchStats hs;
     if (hp) {
@@ -335,16 +385,16 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         hs.max_m = hp->max_m;
         for (int r = 0; r < N_ROUTES; ++r) hs.fwd_count[r] = hp->route_upper[r];
     } else {
-        SW_CUDA(h, cudaMemcpyAsync(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
+        SW_CUDA(h, cudaMemcpyAsync(h->h_stats, stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
         SW_CUDA(h, cudaStreamSynchronize(s));
         hs = *h->h_stats;
     }
     if (hs.malformed) {
-        SW_CUDA(h, cudaMemsetAsync(h->d_hist, 0, NBINS * sizeof(uint32_t), s));  // pack binned some pairs
-        fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, n_pairs);
+        SW_CUDA(h, cudaMemsetAsync(hist, 0, NBINS * sizeof(uint32_t), s));  // pack binned some pairs
+        fill_invalid_kernel<<<std::min<int64_t>((n_pairs + 255) / 256, 4096), 256, 0, s>>>(*out, 0, n_pairs);
         return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
     }
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[2], s));
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[2], s));
 
     // one kernel per route and pass (routes: TAG, S16, S32; sw_common.cuh)
     const void* kfwd[N_ROUTES] = {protein ? (const void*)wavefront_kernel<TS16, WP, KP, false, true>
@@ -389,7 +439,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
                 need = std::max(need, (size_t)std::max(lf[r].blocks * lf[r].warps, lr[r].blocks * lr[r].warps) * segs * 2 * row_bytes);
             }
         }
-        if (need) ENS(scratch, need);
+        if (need) ENS(scratch[slot], need);
     }
 
     // 5. forward binning (length-sorted, longest first)
@@ -397,64 +447,64 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     const int min_rows = std::min(rows16, rows32);
     const bool small_fwd = hs.max_m < BIN_COLS && (hs.max_n + min_rows - 1) / min_rows <= BIN_MAX_STRIPES;
     const bool small_rev = small_fwd && (int64_t)sc.max_sigma * std::min(hs.max_n, hs.max_m) < BIN_COLS;
-    st = bin_order(h, h->order.p, n_pairs, small_fwd, s);
+    st = bin_order(h, h->order.p + lo, lo, hi, small_fwd, slot, s);
     if (st != SW_OK) return st;
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[3], s));
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[3], s));
 
     // 6. forward wavefront
-    SW_CUDA(h, cudaMemsetAsync(h->d_counters, 0, 8 * sizeof(int32_t), s));
+    SW_CUDA(h, cudaMemsetAsync(counters, 0, 8 * sizeof(int32_t), s));
     WaveParams W;
-    W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch.p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
+    W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch[slot].p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
     W.tag_mul = 64;
     W.one = 1;
-    W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p;
-    W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &h->d_stats->swept_fwd; W.counts = h->d_stats->fwd_count;
+    W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p + lo;
+    W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &stats->swept_fwd; W.counts = stats->fwd_count;
     for (int r = 0; r < N_ROUTES; ++r) {
         if (lf[r].blocks <= 0) continue;
         W.route = r;
-        W.item_counter = h->d_counters + r;
+        W.item_counter = counters + r;
         void* args[] = {&W};
         SW_CUDA(h, cudaLaunchKernel(kfwd[r], dim3(lf[r].blocks), dim3(lf[r].warps * 32), args, (size_t)lf[r].smem, s));
         ++h->own_launches;
     }
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[4], s));
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[4], s));
 
     // 7. decode forward keys, prepare the reverse pass
     FinishParams F;
-    F.n_pairs = n_pairs; F.flags = h->flags.p; F.keys_fwd = h->keys_fwd.p; F.keys_rev = h->keys_rev.p;
+    F.lo = lo; F.hi = hi; F.flags = h->flags.p; F.keys_fwd = h->keys_fwd.p; F.keys_rev = h->keys_rev.p;
     F.rcode = h->rcode.p; F.rrev = h->rrev.p;
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
-    F.target = h->target.p; F.key_rev = h->key.p; F.hist = h->d_hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
+    F.target = h->target.p; F.key_rev = h->key.p; F.hist = hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
     F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
-    F.out = *out; F.stats = h->d_stats;
+    F.out = *out; F.stats = stats;
     {
-        const int64_t warps = std::min<int64_t>((n_pairs + FIN_PPW - 1) / FIN_PPW, (int64_t)h->sm_count * 64);
+        const int64_t warps = std::min<int64_t>((hi - lo + FIN_PPW - 1) / FIN_PPW, (int64_t)h->sm_count * 64);
         finish_fwd_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(F);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
     }
-    st = bin_order(h, h->order_rev.p, n_pairs, small_rev, s);
+    st = bin_order(h, h->order_rev.p + lo, lo, hi, small_rev, slot, s);
     if (st != SW_OK) return st;
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[5], s));
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[5], s));
 
     // 8. reverse wavefront on the reversed prefixes
-    W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p;
-    W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &h->d_stats->swept_rev; W.counts = h->d_stats->rev_count;
+    W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p + lo;
+    W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &stats->swept_rev; W.counts = stats->rev_count;
     for (int r = 0; r < N_ROUTES; ++r) {
         if (lr[r].blocks <= 0) continue;
         W.route = r;
-        W.item_counter = h->d_counters + 4 + r;
+        W.item_counter = counters + 4 + r;
         void* args[] = {&W};
         SW_CUDA(h, cudaLaunchKernel(krev[r], dim3(lr[r].blocks), dim3(lr[r].warps * 32), args, (size_t)lr[r].smem, s));
         ++h->own_launches;
     }
-    if (h->timing) SW_CUDA(h, cudaEventRecord(h->ev[6], s));
+    if (timing) SW_CUDA(h, cudaEventRecord(h->ev[6], s));
 
     // 9. starts
-    finish_rev_kernel<<<(int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 16), 256, 0, s>>>(F);
+    finish_rev_kernel<<<(int)std::min<int64_t>((hi - lo + 255) / 256, (int64_t)h->sm_count * 16), 256, 0, s>>>(F);
     SW_CUDA(h, cudaGetLastError());
     ++h->own_launches;
-    if (h->timing) {
+    if (timing) {
         SW_CUDA(h, cudaEventRecord(h->ev[7], s));
         h->ev_valid = true;
     }
@@ -511,26 +561,34 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
     set_smem_attr(wavefront_kernel<TS32, W32, K32, false, false>, big);
     set_smem_attr(wavefront_kernel<TS32, W32, K32, true, false>, big);
     set_smem_attr(bin_scan_kernel, BIN_SCAN_SMEM);
-    if (cudaMalloc(&h->d_stats, sizeof(BatchStats)) != cudaSuccess ||
-        cudaMallocHost(&h->h_stats, sizeof(BatchStats)) != cudaSuccess ||
+    if (cudaMalloc(&h->d_stats, N_SLOTS * sizeof(BatchStats)) != cudaSuccess ||
+        cudaMallocHost(&h->h_stats, N_SLOTS * sizeof(BatchStats)) != cudaSuccess ||
         cudaMallocHost(&h->h_ext, 4 * sizeof(int64_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_counters, 8 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_counters, N_SLOTS * 8 * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_hist, NBINS * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_binbase, NBINS * sizeof(uint32_t)) != cudaSuccess) {
+        cudaMalloc(&h->d_hist, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_binbase, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess) {
         sw_free(h);
         return SW_ERR_OUT_OF_MEMORY;
     }
-    cudaMemset(h->d_stats, 0, sizeof(BatchStats));
-    cudaMemset(h->d_hist, 0, NBINS * sizeof(uint32_t));
+    cudaMemset(h->d_stats, 0, N_SLOTS * sizeof(BatchStats));
+    cudaMemset(h->d_hist, 0, N_SLOTS * NBINS * sizeof(uint32_t));
     for (auto& ev : h->ev) {
         if (cudaEventCreate(&ev) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
     }
-    for (int k = 0; k < 8; ++k) {
+    if (cudaEventCreateWithFlags(&h->ev_prep, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->as_start, cudaEventDisableTiming) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
+    for (int k = 0; k < 2; ++k)
+        if (cudaEventCreateWithFlags(&h->as_in[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->as_comp[k], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&h->as_done[k], cudaEventDisableTiming) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
+    for (int k = 0; k < MAX_CHUNKS; ++k) {
         if (cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
     }
-    if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
+    if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&h->out_stream, cudaStreamNonBlocking) != cudaSuccess) { sw_free(h); return SW_ERR_CUDA; }
     *handle = h;
     return SW_OK;
 }
@@ -576,7 +634,9 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
     double total_cells = 0;
     for (int64_t p = 0; p < n_pairs; ++p)
         total_cells += (double)(q_offsets[p + 1] - q_offsets[p]) * (double)(r_offsets[p + 1] - r_offsets[p]);
-    const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(MAX_CHUNKS, n_pairs / 16384));
+    int want = 4;
+    if (const char* e = std::getenv("SW_HOST_CHUNKS")) want = std::max(1, std::min(MAX_CHUNKS, std::atoi(e)));  // experiments
+    const int n_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(want, n_pairs / 16384));
     int64_t cut[MAX_CHUNKS + 1];
     cut[0] = 0;
     {
@@ -598,12 +658,24 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
         if (rb > ra) SW_CUDA(h, cudaMemcpyAsync(h->st_r.p + (ra - r0), refs + ra, (size_t)(rb - ra), cudaMemcpyHostToDevice, h->copy_stream));
         SW_CUDA(h, cudaEventRecord(h->ev_in[k], h->copy_stream));
     }
+    // the whole batch's workspace first, then chunk k runs on slot k & 1 (caller's stream /
+    // the auxiliary stream), waiting only for its own payload
+    st = prepare_workspace(h, N, (size_t)(qN - q0), (size_t)(rN - r0), sc.alphabet, s);
+    if (st != SW_OK) return st;
+    SW_CUDA(h, cudaEventRecord(h->ev_prep, s));
+    SW_CUDA(h, cudaStreamWaitEvent(h->aux_stream, h->ev_prep, 0));
+    sw_result_t dout;
+    dout.score = h->st_out.p; dout.q_end = h->st_out.p + N; dout.r_end = h->st_out.p + 2 * N;
+    dout.q_start = h->st_out.p + 3 * N; dout.r_start = h->st_out.p + 4 * N;
     sw_status_t result = SW_OK;
     for (int k = 0; k < n_chunks; ++k) {
         const int64_t a = cut[k], b = cut[k + 1];
         if (b <= a) continue;
         HostPlan hp;
-        hp.ext[0] = q_offsets[a]; hp.ext[1] = q_offsets[b]; hp.ext[2] = r_offsets[a]; hp.ext[3] = r_offsets[b];
+        hp.ext[0] = q0; hp.ext[1] = qN; hp.ext[2] = r0; hp.ext[3] = rN;
+        hp.lo = a; hp.hi = b;
+        hp.slot = k & 1;
+        hp.reset_cumulative = k < N_SLOTS;
         hp.max_n = 0; hp.max_m = 0;
         for (int r = 0; r < N_ROUTES; ++r) hp.route_upper[r] = 0;
         for (int64_t p = a; p < b; ++p) {
@@ -617,24 +689,117 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
                             : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
             ++hp.route_upper[route];
         }
-        hp.reset_cumulative = k == 0;
-        SW_CUDA(h, cudaStreamWaitEvent(s, h->ev_in[k], 0));
-        sw_result_t dout;
-        dout.score = h->st_out.p + a; dout.q_end = h->st_out.p + N + a; dout.r_end = h->st_out.p + 2 * N + a;
-        dout.q_start = h->st_out.p + 3 * N + a; dout.r_start = h->st_out.p + 4 * N + a;
-        st = align_impl(h, h->st_q.p - q0, h->st_qo.p + a, h->st_r.p - r0, h->st_ro.p + a, b - a, scoring, &dout, s,
+        cudaStream_t cs = hp.slot ? h->aux_stream : s;
+        SW_CUDA(h, cudaStreamWaitEvent(cs, h->ev_in[k], 0));
+        st = align_impl(h, h->st_q.p - q0, h->st_qo.p, h->st_r.p - r0, h->st_ro.p, n_pairs, scoring, &dout, cs,
                         nullptr, &hp);  // launch counters accumulate over the chunks
         if (st != SW_OK) { result = st; break; }
-        SW_CUDA(h, cudaEventRecord(h->ev_out[k], s));
+        SW_CUDA(h, cudaEventRecord(h->ev_out[k], cs));
         SW_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_out[k], 0));
         for (int f = 0; f < 5; ++f)
             if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f] + a, h->st_out.p + f * N + a, (size_t)(b - a) * 4,
                                                    cudaMemcpyDeviceToHost, h->copy_stream));
     }
     SW_CUDA(h, cudaStreamSynchronize(h->copy_stream));
+    SW_CUDA(h, cudaStreamSynchronize(h->aux_stream));
     SW_CUDA(h, cudaStreamSynchronize(s));
     h->last_stream = s;
     return result;
+}
+
+sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t* q_offsets, const uint8_t* refs,
+                           const int64_t* r_offsets, int64_t n_pairs, const sw_scoring_t* scoring,
+                           const sw_result_t* out_host, void* stream) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (n_pairs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs < 0");
+    if (n_pairs == 0) return SW_OK;
+    if (!queries || !q_offsets || !refs || !r_offsets || !out_host)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+    Scoring sc;
+    bool s16_ok = false;
+    sw_status_t st = check_scoring(h, scoring, sc, s16_ok);
+    if (st != SW_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t N = (size_t)n_pairs;
+    // host-side validation and the plan (reading R15): no device round trip in the pipeline
+    HostPlan hp;
+    hp.lo = 0; hp.hi = n_pairs; hp.slot = 0; hp.reset_cumulative = true;
+    hp.max_n = 0; hp.max_m = 0;
+    for (int r = 0; r < N_ROUTES; ++r) hp.route_upper[r] = 0;
+    const bool tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA);
+    for (int64_t p = 0; p < n_pairs; ++p) {
+        const int64_t n = q_offsets[p + 1] - q_offsets[p], m = r_offsets[p + 1] - r_offsets[p];
+        if (n < 0 || m < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
+        if (n > SW_MAX_SEQ_LEN || m > SW_MAX_SEQ_LEN) continue;  // invalid pair
+        hp.max_n = std::max<int32_t>(hp.max_n, (int32_t)n);
+        hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
+        if (n == 0 || m == 0) continue;
+        const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
+        const int route = (s16_ok && tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
+                        : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
+        ++hp.route_upper[route];
+    }
+    const int64_t q0 = q_offsets[0], qN = q_offsets[n_pairs], r0 = r_offsets[0], rN = r_offsets[n_pairs];
+    hp.ext[0] = q0; hp.ext[1] = qN; hp.ext[2] = r0; hp.ext[3] = rN;
+    const int k = h->as_next;
+    h->as_next ^= 1;
+    // staging slot k: its previous batch must be fully out before it is reused or resized
+    if (h->as_used[k]) {
+        const bool grow = h->as_q[k].cap < (size_t)(qN - q0) + 1 || h->as_r[k].cap < (size_t)(rN - r0) + 1 ||
+                          h->as_qo[k].cap < N + 1 || h->as_out[k].cap < 5 * N;
+        if (grow) SW_CUDA(h, cudaEventSynchronize(h->as_done[k]));
+    }
+#define ENS(buf, n) do { sw_status_t _s = ensure(h, h->buf, (n)); if (_s != SW_OK) return _s; } while (0)
+    ENS(as_q[k], (size_t)(qN - q0) + 1); ENS(as_r[k], (size_t)(rN - r0) + 1);
+    ENS(as_qo[k], N + 1); ENS(as_ro[k], N + 1); ENS(as_out[k], 5 * N);
+#undef ENS
+    // copy-in: the first batch of a pipeline starts after earlier work on the caller's stream
+    // (so events recorded there bracket the whole pipeline); later batches start at once (the
+    // previous batch is still aligning: that is the overlap).  A staging slot is reused only
+    // after its last copy-out.
+    if (!h->as_inflight) {
+        SW_CUDA(h, cudaEventRecord(h->as_start, s));
+        SW_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->as_start, 0));
+    }
+    if (h->as_used[k]) SW_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->as_done[k], 0));
+    SW_CUDA(h, cudaMemcpyAsync(h->as_qo[k].p, q_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, h->copy_stream));
+    SW_CUDA(h, cudaMemcpyAsync(h->as_ro[k].p, r_offsets, (N + 1) * 8, cudaMemcpyHostToDevice, h->copy_stream));
+    if (qN > q0) SW_CUDA(h, cudaMemcpyAsync(h->as_q[k].p, queries + q0, (size_t)(qN - q0), cudaMemcpyHostToDevice, h->copy_stream));
+    if (rN > r0) SW_CUDA(h, cudaMemcpyAsync(h->as_r[k].p, refs + r0, (size_t)(rN - r0), cudaMemcpyHostToDevice, h->copy_stream));
+    SW_CUDA(h, cudaEventRecord(h->as_in[k], h->copy_stream));
+    // align on the caller's stream once the inputs are in (batches in submission order)
+    st = prepare_workspace(h, N, (size_t)(qN - q0), (size_t)(rN - r0), sc.alphabet, s);
+    if (st != SW_OK) return st;
+    SW_CUDA(h, cudaStreamWaitEvent(s, h->as_in[k], 0));
+    sw_result_t dout;
+    int32_t* o = h->as_out[k].p;
+    dout.score = o; dout.q_end = o + N; dout.r_end = o + 2 * N; dout.q_start = o + 3 * N; dout.r_start = o + 4 * N;
+    st = align_impl(h, h->as_q[k].p - q0, h->as_qo[k].p, h->as_r[k].p - r0, h->as_ro[k].p, n_pairs, scoring, &dout, s,
+                    nullptr, &hp);
+    if (st != SW_OK) return st;
+    SW_CUDA(h, cudaEventRecord(h->as_comp[k], s));
+    // results out on their own stream (the copy-in stream keeps feeding the next batch)
+    SW_CUDA(h, cudaStreamWaitEvent(h->out_stream, h->as_comp[k], 0));
+    int32_t* dst[5] = {out_host->score, out_host->q_end, out_host->r_end, out_host->q_start, out_host->r_start};
+    for (int f = 0; f < 5; ++f)
+        if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f], o + f * N, N * 4, cudaMemcpyDeviceToHost, h->out_stream));
+    SW_CUDA(h, cudaEventRecord(h->as_done[k], h->out_stream));
+    h->as_used[k] = true;
+    h->as_inflight = true;
+    h->as_stream = s;
+    h->last_stream = s;
+    return SW_OK;
+}
+
+sw_status_t sw_wait(sw_handle_t h) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    for (int k = 0; k < 2; ++k)
+        if (h->as_used[k]) {
+            SW_CUDA(h, cudaEventSynchronize(h->as_done[k]));
+            if (h->as_stream) SW_CUDA(h, cudaStreamWaitEvent(h->as_stream, h->as_done[k], 0));
+        }
+    h->as_inflight = false;
+    return SW_OK;
 }
 
 sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs) {
@@ -642,14 +807,15 @@ sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs) {
     if (n_bad_pairs) *n_bad_pairs = 0;
     if (!h->have_last) return SW_OK;
     SW_CUDA(h, cudaStreamSynchronize(h->last_stream));
-    SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
-    if (n_bad_pairs) *n_bad_pairs = h->h_stats->n_bad;
-    if (h->h_stats->internal_err) return fail(h, SW_ERR_INTERNAL, "reverse-pass self-check failed");
-    if (h->h_stats->malformed) {
+    BatchStats t;
+    SW_CUDA(h, read_stats(h, t));
+    if (n_bad_pairs) *n_bad_pairs = t.n_bad;
+    if (t.internal_err) return fail(h, SW_ERR_INTERNAL, "reverse-pass self-check failed");
+    if (t.malformed) {
         if (n_bad_pairs) *n_bad_pairs = -1;
         return SW_ERR_BAD_PAIRS;
     }
-    return h->h_stats->n_bad ? SW_ERR_BAD_PAIRS : SW_OK;
+    return t.n_bad ? SW_ERR_BAD_PAIRS : SW_OK;
 }
 
 sw_status_t sw_free(sw_handle_t h) {
@@ -658,9 +824,10 @@ sw_status_t sw_free(sw_handle_t h) {
     cudaDeviceSynchronize();
     release(h->nlen); release(h->mlen); release(h->nlen_rev); release(h->mlen_rev); release(h->target);
     release(h->iota); release(h->order); release(h->order_rev); release(h->qpos); release(h->rpos); release(h->flags);
-    release(h->key); release(h->key_sorted); release(h->cub_temp); release(h->keys_fwd); release(h->keys_rev);
+    release(h->key); release(h->key_sorted);
+    for (int k = 0; k < N_SLOTS; ++k) { release(h->cub_temp[k]); release(h->scratch[k]); } release(h->keys_fwd); release(h->keys_rev);
     release(h->qcode); release(h->rcode); release(h->rrev);
-    release(h->scratch); release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
+    release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
     if (h->d_stats) cudaFree(h->d_stats);
     if (h->h_stats) cudaFreeHost(h->h_stats);
     if (h->h_ext) cudaFreeHost(h->h_ext);
@@ -669,11 +836,21 @@ sw_status_t sw_free(sw_handle_t h) {
     if (h->d_hist) cudaFree(h->d_hist);
     if (h->d_binbase) cudaFree(h->d_binbase);
     for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < MAX_CHUNKS; ++k) {
         if (h->ev_in[k]) cudaEventDestroy(h->ev_in[k]);
         if (h->ev_out[k]) cudaEventDestroy(h->ev_out[k]);
     }
+    if (h->ev_prep) cudaEventDestroy(h->ev_prep);
+    if (h->as_start) cudaEventDestroy(h->as_start);
+    for (int k = 0; k < 2; ++k) {
+        if (h->as_in[k]) cudaEventDestroy(h->as_in[k]);
+        if (h->as_comp[k]) cudaEventDestroy(h->as_comp[k]);
+        if (h->as_done[k]) cudaEventDestroy(h->as_done[k]);
+        release(h->as_q[k]); release(h->as_r[k]); release(h->as_qo[k]); release(h->as_ro[k]); release(h->as_out[k]);
+    }
+    if (h->out_stream) cudaStreamDestroy(h->out_stream);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    if (h->aux_stream) cudaStreamDestroy(h->aux_stream);
     delete h;
     return SW_OK;
 }
@@ -731,17 +908,19 @@ sw_status_t sw_last_launch_count(sw_handle_t h, int32_t* own, int32_t* lib) {
 sw_status_t sw_last_cell_counts(sw_handle_t h, int64_t* fwd, int64_t* swept) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
     if (h->have_last) SW_CUDA(h, cudaStreamSynchronize(h->last_stream));
-    SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
-    if (fwd) *fwd = (int64_t)h->h_stats->cells;
-    if (swept) *swept = (int64_t)h->h_stats->swept_fwd;
+    BatchStats t;
+    SW_CUDA(h, read_stats(h, t));
+    if (fwd) *fwd = (int64_t)t.cells;
+    if (swept) *swept = (int64_t)t.swept_fwd;
     return SW_OK;
 }
 
 sw_status_t sw_last_reverse_cells(sw_handle_t h, int64_t* swept) {
     if (!h || !swept) return SW_ERR_INVALID_ARGUMENT;
     if (h->have_last) SW_CUDA(h, cudaStreamSynchronize(h->last_stream));
-    SW_CUDA(h, cudaMemcpy(h->h_stats, h->d_stats, sizeof(BatchStats), cudaMemcpyDeviceToHost));
-    *swept = (int64_t)h->h_stats->swept_rev;
+    BatchStats t;
+    SW_CUDA(h, read_stats(h, t));
+    *swept = (int64_t)t.swept_rev;
     return SW_OK;
 }
 

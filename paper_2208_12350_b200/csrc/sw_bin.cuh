@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(BIN_SCAN_THREADS) bin_scan_kernel(uint32_t* hi
 }
 
 // order[base[bin(key[p])]++] = p for every pair with work (small-region batches only).
-__global__ void __launch_bounds__(256) bin_scatter_kernel(const uint32_t* key, uint32_t* base, int32_t* order, int64_t n) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) bin_scatter_kernel(const uint32_t* key, uint32_t* base, int32_t* order, int64_t lo,
+                                                         int64_t hi) {
+    for (int64_t p = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = key_bin(key[p]);
         if (b) order[atomicAdd(base + b, 1u)] = (int32_t)p;
     }

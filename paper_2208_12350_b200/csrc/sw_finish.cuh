@@ -9,7 +9,7 @@
 namespace swb {
 
 struct FinishParams {
-    int64_t n_pairs;
+    int64_t lo, hi;                 // pairs of this pass
     const uint8_t* flags;
     const unsigned long long* keys_fwd;
     unsigned long long* keys_rev;   // reverse argmax keys: zeroed by finish_fwd
@@ -57,11 +57,11 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     const uint32_t padw = (uint32_t)P.pad_code * 0x01010101u;
     const uint32_t* src = reinterpret_cast<const uint32_t*>(P.rcode);
     uint32_t* dst = reinterpret_cast<uint32_t*>(P.rrev);
-    for (int64_t base = gw * FIN_PPW; base < P.n_pairs; base += nw * FIN_PPW) {
+    for (int64_t base = P.lo + gw * FIN_PPW; base < P.hi; base += nw * FIN_PPW) {
         const int64_t p = base + lane;
         int64_t rp = 0, w0 = 0;
         int j = -1, cnt = 0;
-        if (lane < FIN_PPW && p < P.n_pairs) {
+        if (lane < FIN_PPW && p < P.hi) {
             P.keys_rev[p] = 0ull;
             const uint8_t fl = P.flags[p];
             const unsigned long long key = P.keys_fwd[p];
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
 // Self-check (pin P14 on the device): the reverse maximum must equal S.
 __global__ void __launch_bounds__(256) finish_rev_kernel(FinishParams P) {
     int err = 0;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.n_pairs; p += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t p = P.lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.hi; p += (int64_t)gridDim.x * blockDim.x) {
         if (P.flags[p] & FLAG_BAD) continue;
         const unsigned long long kf = P.keys_fwd[p];
         if (!kf) continue;
@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(256) finish_rev_kernel(FinishParams P) {
 }
 
 // Whole-batch invalid (malformed offsets): every field -1.
-__global__ void fill_invalid_kernel(sw_result_t out, int64_t n) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+__global__ void fill_invalid_kernel(sw_result_t out, int64_t lo, int64_t hi) {
+    for (int64_t p = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += (int64_t)gridDim.x * blockDim.x) {
         out.score[p] = -1; out.q_end[p] = -1; out.r_end[p] = -1; out.q_start[p] = -1; out.r_start[p] = -1;
     }
 }

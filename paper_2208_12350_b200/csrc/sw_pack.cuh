@@ -31,8 +31,8 @@ struct PackParams {
     const int64_t* q_off;
     const uint8_t* refs;
     const int64_t* r_off;
-    int64_t n_pairs;
-    int64_t q0, qN, r0, rN;      // payload extents (host-read)
+    int64_t lo, hi;              // pairs to pack (positions in the code buffers are batch-global)
+    int64_t q0, qN, r0, rN;      // payload extents of the whole batch (host-read)
     int64_t qshift, rshift;      // (payload + extent start) mod 16: code buffers keep the payload's alignment
     int alphabet;
     int s16_ok;                  // scoring fits the s16x2 path (int8 profile, int16 range)
@@ -190,8 +190,8 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
     int64_t* rdelta = s_rdelta[wib];
     int32_t* sm = s_m[wib];
     int64_t* sqa = s_qa[wib];
-    for (int64_t base = gw * PPW; base < P.n_pairs; base += nw * PPW) {
-        const int cnt = (int)(P.n_pairs - base < PPW ? P.n_pairs - base : (int64_t)PPW);
+    for (int64_t base = P.lo + gw * PPW; base < P.hi; base += nw * PPW) {
+        const int cnt = (int)(P.hi - base < PPW ? P.hi - base : (int64_t)PPW);
         const int64_t p = base + lane;
         const bool act = lane < cnt;
         int64_t qa = 0, qb = 0, ra = 0, rb = 0;

@@ -30,7 +30,7 @@ SW_ALPHABET_PROTEIN = 1
 SW_MAX_SEQ_LEN = 65535
 SW_STAGE_NAMES = ("pack", "sort", "fwd", "mid", "rev", "finish")
 
-EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_batch_status", "sw_free",
+EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
             "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_last_reverse_cells", "sw_dpx_peak")
 
@@ -76,6 +76,8 @@ def load(build_if_missing: bool = True):
     lib.sw_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
     lib.sw_align_batch.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_align_batch_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
+    lib.sw_submit_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
+    lib.sw_wait.argtypes = [vp]
     lib.sw_batch_status.argtypes = [vp, ctypes.POINTER(i64)]
     lib.sw_free.argtypes = [vp]
     lib.sw_status_string.argtypes = [ctypes.c_int]
@@ -150,6 +152,21 @@ def sw_align_batch_host(handle: int, queries, q_offsets, refs, r_offsets, n_pair
     return lib.sw_align_batch_host(ctypes.c_void_p(handle), ctypes.c_void_p(queries), ctypes.c_void_p(q_offsets),
                                    ctypes.c_void_p(refs), ctypes.c_void_p(r_offsets), int(n_pairs),
                                    ctypes.byref(sc), ctypes.byref(res), ctypes.c_void_p(stream))
+
+
+def sw_submit_host(handle: int, queries, q_offsets, refs, r_offsets, n_pairs: int, scoring: dict, out: dict,
+                   stream: int = 0) -> int:
+    """Asynchronous host-buffer batch (include/sw.h): returns once enqueued; sw_wait completes it."""
+    lib = load()
+    sc = make_scoring(scoring)
+    res = sw_result_t(out["score"], out["q_end"], out["r_end"], out["q_start"], out["r_start"])
+    return lib.sw_submit_host(ctypes.c_void_p(handle), ctypes.c_void_p(queries), ctypes.c_void_p(q_offsets),
+                              ctypes.c_void_p(refs), ctypes.c_void_p(r_offsets), int(n_pairs),
+                              ctypes.byref(sc), ctypes.byref(res), ctypes.c_void_p(stream))
+
+
+def sw_wait(handle: int) -> int:
+    return load().sw_wait(ctypes.c_void_p(handle))
 
 
 def sw_batch_status(handle: int) -> tuple[int, int]:

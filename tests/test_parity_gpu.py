@@ -358,3 +358,34 @@ def test_host_entry_point_chunked_pipeline(aligner):
                                 b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS},
                                 torch.cuda.current_stream().cuda_stream)
     assert st == sw.SW_ERR_INVALID_ARGUMENT and (out["score"] == -1).all()
+
+
+def test_submit_host_pipeline_of_batches(aligner):
+    """Asynchronous host-buffer batches (sw_submit_host / sw_wait): several batches in flight on
+    double-buffered staging, growing sizes (staging reallocation while the other slot is busy),
+    DNA and protein, each result equal to the synchronous device entry point."""
+    import torch
+    s = torch.cuda.current_stream().cuda_stream
+    batches = [synth.generate("c1", 0, 300), synth.generate("c2", 0, 3000), synth.generate("c3", 0, 500),
+               synth.generate("c2", 5000, 25000), synth.generate("c1", 0, 1000)]
+    keep = []
+    for b in batches:
+        arrs = (np.ascontiguousarray(b.queries), np.ascontiguousarray(b.q_offsets),
+                np.ascontiguousarray(b.refs), np.ascontiguousarray(b.r_offsets))
+        out = {f: np.full(b.n_pairs, 7, np.int32) for f in FIELDS}
+        st = sw.sw_submit_host(aligner.handle, arrs[0].ctypes.data, arrs[1].ctypes.data, arrs[2].ctypes.data,
+                               arrs[3].ctypes.data, b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS}, s)
+        assert st == sw.SW_OK
+        keep.append((b, arrs, out))
+    assert sw.sw_wait(aligner.handle) == sw.SW_OK
+    for b, _, out in keep:
+        ref = aligner.align(b)
+        for f in FIELDS:
+            np.testing.assert_array_equal(out[f], ref[f])
+    # validation errors come back before anything is enqueued
+    b, arrs, out = keep[0]
+    qo_bad = arrs[1].copy(); qo_bad[3] = qo_bad[5] + 1
+    st = sw.sw_submit_host(aligner.handle, arrs[0].ctypes.data, qo_bad.ctypes.data, arrs[2].ctypes.data,
+                           arrs[3].ctypes.data, b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS}, s)
+    assert st == sw.SW_ERR_INVALID_ARGUMENT
+    assert sw.sw_wait(aligner.handle) == sw.SW_OK

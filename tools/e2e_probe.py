@@ -33,3 +33,6 @@ for _ in range(3): a.align_tensors(q, qo, r, ro, b.scoring, out=out)
 torch.cuda.synchronize()
 e0, e1 = ev(), ev(); e0.record(); a.align_tensors(q, qo, r, ro, b.scoring, out=out); e1.record(); e1.synchronize()
 print("device call ms", e0.elapsed_time(e1))
+import os
+if os.environ.get("SW_PROBE_CHUNKS"):
+    pass
