@@ -14,8 +14,11 @@ A step = one sw_align_batch call (pack, binning, forward wavefront, reverse
 wavefront, finish) over the rank's shard, inputs resident in HBM; L2 (126 MB)
 is flushed between steps (a 512 MB write outside the timed events).  Time =
 sum of per-step CUDA-event times on the call's stream, max over ranks.
-`e2e` repeats the measurement through sw_align_batch_host: pinned host inputs
--> H2D -> align -> D2H of the five result arrays, every step.
+`e2e` repeats the measurement through the public host-buffer API: K batches
+submitted with sw_submit_host (pinned host inputs -> H2D -> align -> D2H of the
+five result arrays, every step; step i+1's copy-in overlaps step i) then
+sw_wait, bracketed by events on the caller's stream; a single synchronous
+sw_align_batch_host call is reported beside it (latency view).
 
 --impl reference runs the CPU oracle (oracle/, plain full-matrix C, all host
 cores) on a bounded sample of the same workload (rank 0 only).
@@ -247,8 +250,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
+    # keep the GPU busy while nvidia-smi starts sampling (warm-up only; not timed)
+    t_end = time.perf_counter() + 1.0
+    while time.perf_counter() < t_end or not clocks.lines:
+        a.align_tensors(q, qo, r, ro, batch.scoring, out=out)
+        torch.cuda.synchronize()
+        if time.perf_counter() > t_end + 5.0:
+            break
+    clocks.lines.clear()
     times, stages = time_device_steps(a, q, qo, r, ro, batch.scoring, out, args.steps, args.warmup, flush_buf, torch)
-    clk = clocks.stop()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -258,36 +268,56 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     total_ms = float(sum(times))
     stage_med = {k: float(np.median([x[k] for x in stages])) for k in stages[0]}
 
-    # ---- e2e through the host entry point (pinned host buffers) ----
+    # ---- e2e through the public host-buffer API (pinned host buffers) ----
+    # K steps as a stream of batches (sw_submit_host / sw_wait): every step copies its inputs
+    # from pinned host memory (75 MB for c2), aligns, and copies the five result arrays back;
+    # step i+1's copy-in overlaps step i's alignment.  Events on the caller's stream bracket
+    # the whole stream (the first copy-in waits for e0, sw_wait joins the last copy-out).
     qh = torch.from_numpy(np.ascontiguousarray(batch.queries)).pin_memory()
     rh = torch.from_numpy(np.ascontiguousarray(batch.refs)).pin_memory()
     qoh = torch.from_numpy(np.ascontiguousarray(batch.q_offsets)).pin_memory()
     roh = torch.from_numpy(np.ascontiguousarray(batch.r_offsets)).pin_memory()
-    outh = torch.empty((5, batch.n_pairs), dtype=torch.int32).pin_memory()
-    ptrs = {f: outh[i].data_ptr() for i, f in enumerate(FIELDS)}
+    outh = [torch.empty((5, batch.n_pairs), dtype=torch.int32).pin_memory() for _ in range(2)]
+    ptrs = [{f: o[i].data_ptr() for i, f in enumerate(FIELDS)} for o in outh]
     s = torch.cuda.current_stream()
 
-    def host_call():
-        rc = sw.sw_align_batch_host(a.handle, qh.data_ptr(), qoh.data_ptr(), rh.data_ptr(), roh.data_ptr(),
-                                    batch.n_pairs, batch.scoring, ptrs, s.cuda_stream)
+    def check(rc):
         if rc != sw.SW_OK:
             raise sw.SWError(rc, sw.sw_last_error_message(a.handle))
 
-    for _ in range(max(1, args.warmup)):
-        host_call()
-    e2e_times = []
-    for _ in range(args.steps):
+    def submit(k):
+        check(sw.sw_submit_host(a.handle, qh.data_ptr(), qoh.data_ptr(), rh.data_ptr(), roh.data_ptr(),
+                                batch.n_pairs, batch.scoring, ptrs[k & 1], s.cuda_stream))
+
+    for k in range(max(1, args.warmup)):
+        submit(k)
+    check(sw.sw_wait(a.handle))
+    flush_buf.zero_()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for k in range(args.steps):
+        submit(k)
+    check(sw.sw_wait(a.handle))
+    e1.record(s)
+    e1.synchronize()
+    e2e_total = float(e0.elapsed_time(e1))
+    # results of the host path must equal the device path
+    same = bool(torch.equal(outh[(args.steps - 1) & 1], out[:, :batch.n_pairs].cpu()))
+    # one synchronous call (sw_align_batch_host: chunked, two streams) for the latency view
+    sync_ms = []
+    for k in range(3):
         flush_buf.zero_()
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        host_call()
-        e1.record(s)
-        e1.synchronize()
-        e2e_times.append(e0.elapsed_time(e1))
-    e2e_total = float(sum(e2e_times))
-    # results of the host path must equal the device path
-    same = bool(torch.equal(outh, out[:, :batch.n_pairs].cpu()))
+        f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(s)
+        check(sw.sw_align_batch_host(a.handle, qh.data_ptr(), qoh.data_ptr(), rh.data_ptr(), roh.data_ptr(),
+                                     batch.n_pairs, batch.scoring, ptrs[0], s.cuda_stream))
+        f1.record(s)
+        f1.synchronize()
+        sync_ms.append(f0.elapsed_time(f1))
+    sync_ms = float(np.median(sync_ms))
+    clk = clocks.stop()  # sampled over the device-timed and the e2e-timed regions
 
     # ---- aggregate over ranks: max time ----
     vals = torch.tensor([total_ms, e2e_total, stage_med["fwd"]], dtype=torch.float64, device=dev)
@@ -361,6 +391,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                      "peak_derived_gcups": round(148 * 2 * 32 * 1.965e9 * 2 / 5.5 / 1e9, 1)},
         "e2e": {"value": round(all_cells * args.steps / (e2e_total * 1e-3) / 1e9, 1), "unit": "GCUPS",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 5 * 4 * batch.n_pairs,
+                "api": "sw_submit_host x steps + sw_wait (pinned host buffers; copy-in of step i+1 overlaps step i)",
+                "ms_per_step": round(e2e_total / args.steps, 4),
+                "single_call_ms": round(sync_ms, 4),
+                "single_call_gcups": round(cells / (sync_ms * 1e-3) / 1e9, 1),
                 "matches_device_path": same},
         "gpu_launches": int(own * args.steps),
         "library_sort_calls": int(lib * args.steps),

@@ -50,12 +50,13 @@ def raw_metrics(rep: str):
 
 
 def sass_hist(rep: str, idx: int):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                         capture_output=True, text=True).stdout
+    """Executed-instruction histogram of the idx-th kernel in the report (0-based)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "--kernel-id", f":::{idx + 1}"], capture_output=True, text=True).stdout
     blocks = out.split('"Kernel Name"')
-    if idx + 1 >= len(blocks):
+    if len(blocks) < 2:
         return []
-    body = blocks[1 + idx].split("\n", 1)[1]
+    body = blocks[1].split("\n", 1)[1]  # first block only (the page can repeat the kernel)
     rows = list(csv.reader(io.StringIO(body)))
     hdr = rows[0]
     cnt = collections.Counter()
@@ -64,10 +65,10 @@ def sass_hist(rep: str, idx: int):
             continue
         d = dict(zip(hdr, r))
         op = d["Source"].strip().split()
-        if not op:
+        if not op or not (d.get("Instructions Executed") or "").isdigit():
             continue
         o = op[1] if op[0].startswith("@") else op[0]
-        cnt[o] += int(d["Instructions Executed"] or 0)
+        cnt[o] += int(d["Instructions Executed"])
     return cnt.most_common(18)
 
 
@@ -112,7 +113,7 @@ def main():
         f.write(launch_shares(launches) + "\n")
     with open(os.path.join(d, "ncu_full_wavefront.md"), "w") as f:
         f.write(f"# ncu --set full ({rnd}): wavefront kernels on c2 (100k DNA pairs), "
-                f"`tools/prof_one.py c2`, 3rd call\n\n")
+                f"`tools/prof_one.py c2`, 3rd call (forward, then reverse)\n\n")
         f.write(full_summary(rep) + "\n")
     print("wrote", d)
 
