@@ -340,6 +340,15 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                           "ms": round(med, 3), "fwd_kernel_gcups": round(bx.cells() / float(np.median([x["fwd"] for x in sx])) / 1e6, 1),
                           "stage_ms": {k: round(float(np.median([x[k] for x in sx])), 4) for k in sx[0]}}
 
+    if rank == 0 and not args.no_extra:
+        # forward pass only (SW_MODE_END_ONLY: score, q_end, r_end), the same shard
+        a.set_mode(sw.SW_MODE_END_ONLY)
+        te, se = time_device_steps(a, q, qo, r, ro, batch.scoring, out, 5, 2, flush_buf, torch)
+        a.set_mode(sw.SW_MODE_FULL)
+        med = float(np.median(te))
+        extra["end_only"] = {"workload": "rank-0 shard, SW_MODE_END_ONLY (forward pass only)", "ms": round(med, 3),
+                             "gcups": round(cells / med / 1e6, 1)}
+
     cpu = None
     parity = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -86,6 +86,17 @@ typedef struct {
     int32_t* r_start;
 } sw_result_t;
 
+/*
+ * Pass selection (the paper's V0-style one-kernel
+ * mode): SW_MODE_FULL (default) runs the forward and the
+ * reverse pass; SW_MODE_END_ONLY runs the forward pass only -- score, q_end
+ * and r_end are exact as in FULL mode, q_start / r_start are not written (the
+ * sw_result_t pointers may then be NULL).  Applies to every later call on
+ * the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown mode.
+ */
+typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1 } sw_mode_t;
+sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
+
 /* Create a handle bound to CUDA device `device`.  Allocates no large memory;
  * the workspace grows on demand and is reused across calls. */
 sw_status_t sw_init(sw_handle_t* handle, int device);

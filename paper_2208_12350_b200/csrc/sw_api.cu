@@ -99,6 +99,7 @@ struct sw_context {
     cudaStream_t copy_stream = nullptr;  // host-buffer entry point: overlapped copies
     cudaEvent_t ev_in[MAX_CHUNKS] = {}, ev_out[MAX_CHUNKS] = {}, ev_prep = nullptr;
     bool timing = false;
+    int mode = SW_MODE_FULL;
     cudaEvent_t ev[8] = {};
     bool ev_valid = false;
     int32_t own_launches = 0, lib_launches = 0;
@@ -314,8 +315,9 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     int32_t* counters = h->d_counters + slot * 8;
     h->ev_valid = false;
     if (n_pairs == 0) return SW_OK;
+    const bool end_only = h->mode == SW_MODE_END_ONLY;
     if (!queries || !q_off || !refs || !r_off || !out || !out->score || !out->q_end || !out->r_end ||
-        !out->q_start || !out->r_start)
+        (!end_only && (!out->q_start || !out->r_start)))
         return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
     h->last_stream = s;
     h->have_last = true;
@@ -476,12 +478,19 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
     F.target = h->target.p; F.key_rev = h->key.p; F.hist = hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
     F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
-    F.out = *out; F.stats = stats;
+    F.out = *out; F.stats = stats; F.end_only = end_only ? 1 : 0;
     {
         const int64_t warps = std::min<int64_t>((hi - lo + FIN_PPW - 1) / FIN_PPW, (int64_t)h->sm_count * 64);
         finish_fwd_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(F);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
+    }
+    if (end_only) {  // forward pass only (sw_set_mode)
+        if (timing) {
+            for (int k = 5; k < 8; ++k) SW_CUDA(h, cudaEventRecord(h->ev[k], s));
+            h->ev_valid = true;
+        }
+        return SW_OK;
     }
     st = bin_order(h, h->order_rev.p + lo, lo, hi, small_rev, slot, s);
     if (st != SW_OK) return st;
@@ -696,7 +705,7 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
         if (st != SW_OK) { result = st; break; }
         SW_CUDA(h, cudaEventRecord(h->ev_out[k], cs));
         SW_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_out[k], 0));
-        for (int f = 0; f < 5; ++f)
+        for (int f = 0; f < (h->mode == SW_MODE_END_ONLY ? 3 : 5); ++f)
             if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f] + a, h->st_out.p + f * N + a, (size_t)(b - a) * 4,
                                                    cudaMemcpyDeviceToHost, h->copy_stream));
     }
@@ -705,6 +714,13 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
     SW_CUDA(h, cudaStreamSynchronize(s));
     h->last_stream = s;
     return result;
+}
+
+sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (mode != SW_MODE_FULL && mode != SW_MODE_END_ONLY) return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
+    h->mode = mode;
+    return SW_OK;
 }
 
 sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t* q_offsets, const uint8_t* refs,
@@ -781,7 +797,7 @@ sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t*
     // results out on their own stream (the copy-in stream keeps feeding the next batch)
     SW_CUDA(h, cudaStreamWaitEvent(h->out_stream, h->as_comp[k], 0));
     int32_t* dst[5] = {out_host->score, out_host->q_end, out_host->r_end, out_host->q_start, out_host->r_start};
-    for (int f = 0; f < 5; ++f)
+    for (int f = 0; f < (h->mode == SW_MODE_END_ONLY ? 3 : 5); ++f)
         if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f], o + f * N, N * 4, cudaMemcpyDeviceToHost, h->out_stream));
     SW_CUDA(h, cudaEventRecord(h->as_done[k], h->out_stream));
     h->as_used[k] = true;

@@ -25,6 +25,7 @@ struct FinishParams {
     int rows_s16, rows_s32;
     int max_sigma, gap_extend;
     uint8_t pad_code;
+    int end_only;                   // forward pass only: no start outputs, no reverse-pass preparation
     sw_result_t out;
     BatchStats* stats;
 };
@@ -69,12 +70,14 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
             if (key) decode_key(key, S, j, i);
             if (fl & FLAG_BAD) {
                 P.out.score[p] = -1; P.out.q_end[p] = -1; P.out.r_end[p] = -1;
-                P.out.q_start[p] = -1; P.out.r_start[p] = -1;
+                if (!P.end_only) { P.out.q_start[p] = -1; P.out.r_start[p] = -1; }
                 P.key_rev[p] = 0;
             } else if (S == 0) {
                 P.out.score[p] = 0; P.out.q_end[p] = -1; P.out.r_end[p] = -1;
-                P.out.q_start[p] = -1; P.out.r_start[p] = -1;
+                if (!P.end_only) { P.out.q_start[p] = -1; P.out.r_start[p] = -1; }
                 P.key_rev[p] = 0;
+            } else if (P.end_only) {
+                P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
             } else {
                 P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
                 const int n2 = i + 1;
@@ -194,7 +197,9 @@ __global__ void __launch_bounds__(256) finish_rev_kernel(FinishParams P) {
 // Whole-batch invalid (malformed offsets): every field -1.
 __global__ void fill_invalid_kernel(sw_result_t out, int64_t lo, int64_t hi) {
     for (int64_t p = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += (int64_t)gridDim.x * blockDim.x) {
-        out.score[p] = -1; out.q_end[p] = -1; out.r_end[p] = -1; out.q_start[p] = -1; out.r_start[p] = -1;
+        out.score[p] = -1; out.q_end[p] = -1; out.r_end[p] = -1;
+        if (out.q_start) out.q_start[p] = -1;
+        if (out.r_start) out.r_start[p] = -1;
     }
 }
 

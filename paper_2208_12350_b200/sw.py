@@ -29,8 +29,10 @@ SW_ALPHABET_DNA = 0
 SW_ALPHABET_PROTEIN = 1
 SW_MAX_SEQ_LEN = 65535
 SW_STAGE_NAMES = ("pack", "sort", "fwd", "mid", "rev", "finish")
+SW_MODE_FULL = 0
+SW_MODE_END_ONLY = 1
 
-EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_batch_status", "sw_free",
+EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
             "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_last_reverse_cells", "sw_dpx_peak")
 
@@ -78,6 +80,7 @@ def load(build_if_missing: bool = True):
     lib.sw_align_batch_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_submit_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_wait.argtypes = [vp]
+    lib.sw_set_mode.argtypes = [vp, ctypes.c_int32]
     lib.sw_batch_status.argtypes = [vp, ctypes.POINTER(i64)]
     lib.sw_free.argtypes = [vp]
     lib.sw_status_string.argtypes = [ctypes.c_int]
@@ -271,6 +274,12 @@ class Aligner:
         a, b = ctypes.c_int32(0), ctypes.c_int32(0)
         load().sw_last_launch_count(ctypes.c_void_p(self.handle), ctypes.byref(a), ctypes.byref(b))
         return a.value, b.value
+
+    def set_mode(self, mode: int):
+        """SW_MODE_FULL (forward + reverse) or SW_MODE_END_ONLY (forward only; starts not written)."""
+        st = load().sw_set_mode(ctypes.c_void_p(self.handle), int(mode))
+        if st != SW_OK:
+            raise SWError(st, sw_last_error_message(self.handle))
 
     def reverse_cells(self):
         a = ctypes.c_int64(0)

@@ -389,3 +389,29 @@ def test_submit_host_pipeline_of_batches(aligner):
                            arrs[3].ctypes.data, b.n_pairs, b.scoring, {f: out[f].ctypes.data for f in FIELDS}, s)
     assert st == sw.SW_ERR_INVALID_ARGUMENT
     assert sw.sw_wait(aligner.handle) == sw.SW_OK
+
+
+def test_end_only_mode(aligner):
+    """SW_MODE_END_ONLY (forward pass only): score / q_end / r_end identical to the
+    oracle, start arrays untouched, NULL start pointers accepted; FULL mode restores starts."""
+    import torch
+    b = synth.generate("c2", 0, 4000)
+    exp = oracle_batch(b)
+    q, qo, r, ro = aligner.to_device(b)
+    out = torch.full((5, b.n_pairs), 12345, dtype=torch.int32, device="cuda:0")
+    aligner.set_mode(sw.SW_MODE_END_ONLY)
+    try:
+        res = sw.sw_result_t(out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(), 0, 0)
+        st = sw.load().sw_align_batch(aligner.handle, q.data_ptr(), qo.data_ptr(), r.data_ptr(), ro.data_ptr(),
+                                      b.n_pairs, sw.make_scoring(b.scoring), res, torch.cuda.current_stream().cuda_stream)
+        assert st == sw.SW_OK
+        torch.cuda.synchronize()
+        o = out.cpu().numpy()
+        for i, f in enumerate(FIELDS[:3]):
+            np.testing.assert_array_equal(o[i], exp[f])
+        assert (o[3] == 12345).all() and (o[4] == 12345).all()
+    finally:
+        aligner.set_mode(sw.SW_MODE_FULL)
+    got = aligner.align(b)
+    for f in FIELDS:
+        np.testing.assert_array_equal(got[f], exp[f])
