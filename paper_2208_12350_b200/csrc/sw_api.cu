@@ -694,7 +694,7 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
             hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
             if (n == 0 || m == 0) continue;
             const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
-            const int route = (s16_ok && tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
+            const int route = (s16_ok && tag_ok && (int64_t)sc.max_sigma * n <= TAG_MAX_SCORE) ? ROUTE_TAG
                             : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
             ++hp.route_upper[route];
         }
@@ -751,7 +751,7 @@ sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t*
         hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
         if (n == 0 || m == 0) continue;
         const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
-        const int route = (s16_ok && tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
+        const int route = (s16_ok && tag_ok && (int64_t)sc.max_sigma * n <= TAG_MAX_SCORE) ? ROUTE_TAG
                         : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
         ++hp.route_upper[route];
     }

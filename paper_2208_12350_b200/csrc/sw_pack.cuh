@@ -322,7 +322,9 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
                 nn = (int)n; mm = (int)m;
                 // largest score the pair can reach (reading R13): picks the lane width
                 const int64_t smax = (int64_t)P.max_sigma * (int64_t)min(nn, mm);
-                const int route = (P.s16_ok && P.tag_ok && smax <= TAG_MAX_SCORE) ? ROUTE_TAG
+                // TAG: every cell a sweep over this query can compute (also past the reference, in
+                // the columns of a longer reference of the work item) has H <= max_s * n <= 511
+                const int route = (P.s16_ok && P.tag_ok && (int64_t)P.max_sigma * nn <= TAG_MAX_SCORE) ? ROUTE_TAG
                                 : (P.s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
                 fl = route_flag(route);
                 if (nn > 0 && mm > 0) {

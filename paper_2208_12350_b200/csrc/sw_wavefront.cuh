@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
     // Row/column tags (H*64 + tag) need H <= 511 in every computed cell, also past a half's
-    // reference: forward items without end events (the columns past a reference are pad
-    // codes) and reverse items with max_s * rows <= 511 (finish_fwd routes the rest to S16).
+    // reference: the TAG route takes pairs with max_s * n <= 511 (pack), which bounds every
+    // cell of the query's rows whatever the columns hold (end events, reverse pass alike).
     constexpr bool TAGF = TAG;
     extern __shared__ __align__(16) uint8_t smem[];
     // substitution table for the profile builds, in shared memory: lanes index it with
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
             // ---- the stripe's column sweep (single-stripe items skip all hand-off code) ----
             if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, false, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, true, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
                 else
                     steps += sweep<T, W, K, REV, false, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const Wav
                 uint2* scr_out = reinterpret_cast<uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, true, true, false>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, true, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
                 else
                     steps += sweep<T, W, K, REV, true, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
