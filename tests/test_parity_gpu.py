@@ -115,6 +115,31 @@ def test_c2_full_size_sampled(aligner):
     assert np.all(got["score"] > 0)
 
 
+def test_c4_per_gpu_share_sampled(aligner):
+    """C4 (4M pairs) at 8 GPUs gives each GPU 500k pairs: one such call, 300 sampled pairs vs the oracle."""
+    b = synth.generate("c4", 3_500_000, 4_000_000)
+    got = aligner.align(b)
+    rng = np.random.default_rng(4)
+    idx = np.sort(rng.choice(b.n_pairs, size=300, replace=False))
+    sub = b.subset(idx)
+    assert_parity({f: got[f][idx] for f in FIELDS}, oracle_batch(sub), sub)
+
+
+def test_c5_full_size_sampled(aligner):
+    """C5 at its full size (400k pairs, references up to 16 kb, queries up to 4 kb) in one call;
+    short and long sampled pairs vs the oracle (long ones bounded in oracle cost)."""
+    b = synth.generate("c5")
+    got = aligner.align(b)
+    n = np.diff(b.q_offsets); m = np.diff(b.r_offsets)
+    rng = np.random.default_rng(5)
+    short = rng.choice(np.nonzero(n == 150)[0], size=150, replace=False)
+    longs = np.nonzero((n > 150) & (n * m < 4e7))[0]
+    long_pick = rng.choice(longs, size=min(30, longs.size), replace=False)
+    idx = np.sort(np.concatenate([short, long_pick]))
+    sub = b.subset(idx)
+    assert_parity({f: got[f][idx] for f in FIELDS}, oracle_batch(sub), sub)
+
+
 # ------------------------------------------------------------ adversarial
 
 def test_tie_heavy_low_entropy(aligner):
