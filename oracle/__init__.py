@@ -72,6 +72,8 @@ def _load():
         lib.oracle_align_batch.argtypes = [u8p, i64p, u8p, i64p, ctypes.c_int64, sp,
                                            i32p, i32p, i32p, i32p, i32p, ctypes.c_int]
         lib.oracle_align_batch.restype = ctypes.c_int
+        lib.oracle_traceback.argtypes = [u8p, ctypes.c_int64, u8p, ctypes.c_int64, sp, i32p, ctypes.c_char_p]
+        lib.oracle_traceback.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -118,6 +120,39 @@ def align(q, r, sc) -> tuple:
     if st in (NO_MEMORY, REVERSE_MISMATCH):
         raise RuntimeError(f"oracle failure status {st}")
     return tuple(int(x) for x in out)
+
+
+def traceback(q, r, sc, res=None) -> str | None:
+    """Alignment ops ('M' aligned pair, 'I' query residue vs gap, 'D' reference residue vs gap)
+    from start to end of the pair's reported alignment (sw_oracle.c oracle_traceback, reading R20).
+    '' for S == 0, None for an invalid pair.  ``res`` = align(q, r, sc) if already known."""
+    lib = _load()
+    qa, ra = _u8(q), _u8(r)
+    if res is None:
+        res = align(qa, ra, sc)
+    qa_b = qa if qa.size else np.zeros(1, np.uint8)
+    ra_b = ra if ra.size else np.zeros(1, np.uint8)
+    rv = np.asarray(res, dtype=np.int32)
+    buf = ctypes.create_string_buffer(max(1, qa.size + ra.size))
+    k = lib.oracle_traceback(_ptr(qa_b, ctypes.c_uint8), qa.size, _ptr(ra_b, ctypes.c_uint8), ra.size,
+                             ctypes.byref(_as_scoring(sc)), _ptr(rv, ctypes.c_int32), buf)
+    if k == -2:
+        raise RuntimeError("oracle traceback: global optimum differs from S")
+    if k < 0:
+        return None
+    return buf.raw[:k].decode()
+
+
+def cigar(ops: str) -> str:
+    """Run-length form of an op string ('MMMID' -> '3M1I1D')."""
+    out, k = [], 0
+    while k < len(ops):
+        t = k
+        while t < len(ops) and ops[t] == ops[k]:
+            t += 1
+        out.append(f"{t - k}{ops[k]}")
+        k = t
+    return "".join(out)
 
 
 def fill_H(q, r, sc) -> np.ndarray:

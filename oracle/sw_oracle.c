@@ -273,6 +273,122 @@ done:
     return st;
 }
 
+/* ------------------------------------------------------------- traceback */
+
+/*
+ * Alignment path of a pair (reading R20).
+ * Given the pair's (S, q_end, r_end, q_start, r_start) from oracle_align with
+ * S > 0, the path is an optimal GLOBAL affine alignment of the substrings
+ * A = q[q_start..q_end] and B = r[r_start..r_end] (its score equals S: it is a
+ * local alignment, so <= S, and the reported alignment is one, so >= S), taken
+ * by the traceback of PAPER.md:153 / 165 ("tracing back from the highest
+ * score") from the bottom-right cell.  Among all optimal alignments it is the
+ * one whose op string, read from the end, is lexicographically greatest with
+ * M > I > D -- SPEC.md:395/464's diagonal > up > left, where 'M' is an aligned
+ * pair, 'I' a query residue against a gap (vertical, state F) and 'D' a
+ * reference residue against a gap (horizontal, state E).  As a state machine:
+ *   H state: diagonal optimal -> 'M'; else H == F -> F state; else E state.
+ *   F state ('I', consuming query row i): go back to H if the gap opened here
+ *     and the cell above prefers the diagonal (next op 'M'); else stay in F if
+ *     the gap extends here or the cell above prefers F (next op 'I'); else H.
+ *   E state ('D', consuming reference column j): back to H if the gap opened
+ *     here and the cell to the left prefers the diagonal or F (next op 'M' or
+ *     'I'); else stay in E (next op 'D').
+ * Global recurrence (no 0 term; gap of length k scores o + (k-1) e, R1):
+ *   H[0][0] = 0, H[i][0] = F[i][0] = o + (i-1) e, H[0][j] = E[0][j] = o + (j-1) e
+ *   E[i][j] = max(E[i][j-1] + e, H[i][j-1] + o)
+ *   F[i][j] = max(F[i-1][j] + e, H[i-1][j] + o)
+ *   H[i][j] = max(H[i-1][j-1] + s(A_i, B_j), E[i][j], F[i][j])
+ * ops (a + b bytes capacity) receives the ops from start to end; returns the
+ * number of ops, 0 for S == 0, -1 for an invalid pair or scoring, -2 if the
+ * global optimum differs from S (must never happen).
+ */
+#define ORACLE_NEG_INF (-(1 << 28))
+int oracle_traceback(const uint8_t* qs, int64_t n, const uint8_t* rs, int64_t m, const oracle_scoring* sc,
+                     const int32_t res[5], char* ops)
+{
+    if (oracle_check_scoring(sc)) return -1;
+    const int32_t S = res[0];
+    if (S < 0) return -1;
+    if (S == 0) return 0;
+    const int64_t q0 = res[3], q1 = res[1], r0 = res[4], r1 = res[2];
+    if (q0 < 0 || r0 < 0 || q1 < q0 || r1 < r0 || q1 >= n || r1 >= m) return -1;
+    const int64_t a = q1 - q0 + 1, b = r1 - r0 + 1;
+    int* A = (int*)malloc(sizeof(int) * (size_t)a);
+    int* B = (int*)malloc(sizeof(int) * (size_t)b);
+    size_t cells = (size_t)(a + 1) * (size_t)(b + 1);
+    int32_t* H = (int32_t*)malloc(sizeof(int32_t) * cells);
+    int32_t* E = (int32_t*)malloc(sizeof(int32_t) * cells);
+    int32_t* F = (int32_t*)malloc(sizeof(int32_t) * cells);
+    char* rev = (char*)malloc((size_t)(a + b));
+    int ret = -1;
+    if (!A || !B || !H || !E || !F || !rev) goto done;
+    for (int64_t i = 0; i < a; ++i) if ((A[i] = oracle_code(sc->alphabet, qs[q0 + i])) < 0) goto done;
+    for (int64_t j = 0; j < b; ++j) if ((B[j] = oracle_code(sc->alphabet, rs[r0 + j])) < 0) goto done;
+    {
+        const int32_t o = sc->gap_open, e = sc->gap_extend;
+#define AT(X, i, j) X[(size_t)(i) * (size_t)(b + 1) + (size_t)(j)]
+        AT(H, 0, 0) = 0; AT(E, 0, 0) = ORACLE_NEG_INF; AT(F, 0, 0) = ORACLE_NEG_INF;
+        for (int64_t j = 1; j <= b; ++j) {
+            AT(H, 0, j) = o + (int32_t)(j - 1) * e; AT(E, 0, j) = AT(H, 0, j); AT(F, 0, j) = ORACLE_NEG_INF;
+        }
+        for (int64_t i = 1; i <= a; ++i) {
+            AT(H, i, 0) = o + (int32_t)(i - 1) * e; AT(F, i, 0) = AT(H, i, 0); AT(E, i, 0) = ORACLE_NEG_INF;
+            for (int64_t j = 1; j <= b; ++j) {
+                int32_t ev = AT(E, i, j - 1) + e, eo = AT(H, i, j - 1) + o;
+                int32_t fv = AT(F, i - 1, j) + e, fo = AT(H, i - 1, j) + o;
+                AT(E, i, j) = ev > eo ? ev : eo;
+                AT(F, i, j) = fv > fo ? fv : fo;
+                int32_t d = AT(H, i - 1, j - 1) + oracle_sigma(sc, A[i - 1], B[j - 1]);
+                int32_t h = d;
+                if (AT(F, i, j) > h) h = AT(F, i, j);
+                if (AT(E, i, j) > h) h = AT(E, i, j);
+                AT(H, i, j) = h;
+            }
+        }
+        if (AT(H, a, b) != S) { ret = -2; goto done; }
+        /* preferred move out of H at (i, j): 0 diagonal, 1 F (vertical), 2 E (horizontal) */
+#define h_pref(ii, jj) ((ii) > 0 && (jj) > 0 && AT(H, ii, jj) == AT(H, (ii) - 1, (jj) - 1) + oracle_sigma(sc, A[(ii) - 1], B[(jj) - 1]) ? 0 \
+                        : ((ii) > 0 && AT(H, ii, jj) == AT(F, ii, jj)) ? 1 : 2)
+        /* traceback from (a, b) in state H */
+        int64_t i = a, j = b, k = 0;
+        int state = 0; /* 0 = H, 1 = F (vertical), 2 = E (horizontal) */
+        while (i > 0 || j > 0) {
+            if (state == 0) {
+                if (i > 0 && j > 0 && AT(H, i, j) == AT(H, i - 1, j - 1) + oracle_sigma(sc, A[i - 1], B[j - 1])) {
+                    rev[k++] = 'M'; --i; --j;
+                } else if (i > 0 && AT(H, i, j) == AT(F, i, j)) {
+                    state = 1;
+                } else {
+                    state = 2;
+                }
+            } else if (state == 1) {
+                rev[k++] = 'I';
+                const int open = AT(F, i, j) == AT(H, i - 1, j) + o;
+                const int ext = AT(F, i, j) == AT(F, i - 1, j) + e;
+                const int up = h_pref(i - 1, j);
+                if (open && up == 0) state = 0;
+                else if (ext || (open && up == 1)) state = 1;
+                else state = 0;
+                --i;
+            } else {
+                rev[k++] = 'D';
+                const int open = AT(E, i, j) == AT(H, i, j - 1) + o;
+                const int left = h_pref(i, j - 1);
+                state = (open && left != 2) ? 0 : 2;
+                --j;
+            }
+        }
+#undef h_pref
+#undef AT
+        for (int64_t t = 0; t < k; ++t) ops[t] = rev[k - 1 - t];
+        ret = (int)k;
+    }
+done:
+    free(A); free(B); free(H); free(E); free(F); free(rev);
+    return ret;
+}
+
 /* ------------------------------------------------------------------ batch */
 
 typedef struct {
