@@ -348,6 +348,25 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         med = float(np.median(te))
         extra["end_only"] = {"workload": "rank-0 shard, SW_MODE_END_ONLY (forward pass only)", "ms": round(med, 3),
                              "gcups": round(cells / med / 1e6, 1)}
+        # alignment paths of the same shard (sw_traceback) after the full alignment
+        a.align_tensors(q, qo, r, ro, batch.scoring, out=out)
+        ops, n_ops = a.traceback_tensors(q, qo, r, ro, batch.scoring, out)
+        torch.cuda.synchronize()
+        tt = []
+        for _ in range(5):
+            g0 = torch.cuda.Event(enable_timing=True); g1 = torch.cuda.Event(enable_timing=True)
+            g0.record()
+            a.traceback_tensors(q, qo, r, ro, batch.scoring, out, ops, n_ops)
+            g1.record()
+            g1.synchronize()
+            tt.append(g0.elapsed_time(g1))
+        o5 = out[:, :batch.n_pairs].cpu().numpy().astype(np.int64)
+        icells = int(np.sum(np.where(o5[0] > 0, (o5[1] - o5[3] + 1) * (o5[2] - o5[4] + 1), 0)))
+        med = float(np.median(tt))
+        extra["traceback"] = {"workload": "rank-0 shard, sw_traceback after sw_align_batch", "ms": round(med, 3),
+                              "interval_cells": icells, "interval_gcups": round(icells / med / 1e6, 1),
+                              "pairs_per_s": round(batch.n_pairs / med * 1e3, 1),
+                              "ops_total": int(n_ops[:batch.n_pairs].clamp(min=0).sum().item())}
 
     cpu = None
     parity = None

@@ -97,6 +97,31 @@ typedef struct {
 typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1 } sw_mode_t;
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
 
+/*
+ * Alignment paths (reading R20).  For a
+ * batch already aligned with sw_align_batch / sw_align_batch_host (the same
+ * inputs; `res` = its five result arrays in DEVICE memory, full mode), write
+ * each pair's alignment as ops from start to end: 'M' an aligned pair, 'I' a
+ * query residue against a gap, 'D' a reference residue against a gap.  The
+ * path is the optimal global affine alignment of q[q_start..q_end] and
+ * r[r_start..r_end] (its score is the pair's S); among several, the one whose
+ * op string read from the end is lexicographically greatest with M > I > D
+ * (SPEC.md's diagonal > up > left traceback).
+ *   queries .. r_offsets, n_pairs, scoring   as for sw_align_batch (DEVICE)
+ *   ops     DEVICE uint8, (q_offsets[n]-q_offsets[0]) + (r_offsets[n]-r_offsets[0])
+ *           bytes; pair p's ops start at (q_offsets[p]-q_offsets[0]) +
+ *           (r_offsets[p]-r_offsets[0]) (a path has at most n_p + m_p ops)
+ *   n_ops   DEVICE int32[n_pairs]: op count; 0 when S == 0; -1 for an invalid
+ *           pair (score -1)
+ * Enqueued on `stream`; synchronises on it once (the batch's largest interval
+ * sizes the scratch: one direction word per 5 cells of it per resident warp).
+ */
+sw_status_t sw_traceback(sw_handle_t h,
+                         const uint8_t* queries, const int64_t* q_offsets,
+                         const uint8_t* refs, const int64_t* r_offsets,
+                         int64_t n_pairs, const sw_scoring_t* scoring,
+                         const sw_result_t* res, uint8_t* ops, int32_t* n_ops, void* stream);
+
 /* Create a handle bound to CUDA device `device`.  Allocates no large memory;
  * the workspace grows on demand and is reused across calls. */
 sw_status_t sw_init(sw_handle_t* handle, int device);

@@ -17,6 +17,7 @@
 #include "sw_pack.cuh"
 #include "sw_wavefront.cuh"
 #include "sw_finish.cuh"
+#include "sw_traceback.cuh"
 
 using namespace swb;
 
@@ -84,6 +85,11 @@ struct sw_context {
     DevBuf<uint8_t> st_q, st_r;
     DevBuf<int64_t> st_qo, st_ro;
     DevBuf<int32_t> st_out;
+    // alignment paths (sw_traceback): per-warp direction words and stripe boundary rows
+    DevBuf<uint32_t> tb_dir;
+    DevBuf<int2> tb_bnd;
+    int32_t* d_tb = nullptr;   // [0] max a, [1] max b, [2] queue head, [3] internal errors; then int64 q0, r0
+    int32_t* h_tb = nullptr;   // pinned copy
     // asynchronous host-buffer entry point: double-buffered staging, copy-in / copy-out streams
     DevBuf<uint8_t> as_q[2], as_r[2];
     DevBuf<int64_t> as_qo[2], as_ro[2];
@@ -576,7 +582,9 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
         cudaMalloc(&h->d_counters, N_SLOTS * 8 * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_hist, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_binbase, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess) {
+        cudaMalloc(&h->d_binbase, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_tb, 8 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMallocHost(&h->h_tb, 8 * sizeof(int32_t)) != cudaSuccess) {
         sw_free(h);
         return SW_ERR_OUT_OF_MEMORY;
     }
@@ -716,6 +724,59 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
     return result;
 }
 
+sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q_offsets, const uint8_t* refs,
+                         const int64_t* r_offsets, int64_t n_pairs, const sw_scoring_t* scoring, const sw_result_t* res,
+                         uint8_t* ops, int32_t* n_ops, void* stream) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (n_pairs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_pairs < 0");
+    if (n_pairs == 0) return SW_OK;
+    if (!queries || !q_offsets || !refs || !r_offsets || !res || !res->score || !res->q_end || !res->r_end ||
+        !res->q_start || !res->r_start || !ops || !n_ops)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
+    int dev = -1;
+    SW_CUDA(h, cudaGetDevice(&dev));
+    if (dev != h->device) return fail(h, SW_ERR_WRONG_DEVICE, "current device differs from the handle's device");
+    Scoring sc;
+    bool s16_ok = false;
+    sw_status_t st = check_scoring(h, scoring, sc, s16_ok);
+    if (st != SW_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    // 1. the batch's largest interval (sizes the per-warp scratch) and the offset bases
+    SW_CUDA(h, cudaMemsetAsync(h->d_tb, 0, 4 * sizeof(int32_t), s));
+    int64_t* base = reinterpret_cast<int64_t*>(h->d_tb + 4);
+    trace_extent_kernel<<<(int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 8), 256, 0, s>>>(
+        *res, n_pairs, q_offsets, r_offsets, h->d_tb, base);
+    SW_CUDA(h, cudaGetLastError());
+    SW_CUDA(h, cudaMemcpyAsync(h->h_tb, h->d_tb, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SW_CUDA(h, cudaStreamSynchronize(s));
+    const int32_t max_a = h->h_tb[0], max_b = h->h_tb[1];
+    const int64_t q0 = reinterpret_cast<int64_t*>(h->h_tb + 4)[0], r0 = reinterpret_cast<int64_t*>(h->h_tb + 4)[1];
+    // 2. one warp per pair; the warp count is capped so the direction scratch stays <= 4 GiB
+    const int64_t ns = std::max<int64_t>(1, ((int64_t)max_a + TB_ROWS - 1) / TB_ROWS);
+    const int64_t dir_words = ns * ((int64_t)max_b + 31) * 32;
+    const int64_t bnd_len = (int64_t)max_b + 1;
+    const int64_t budget_words = ((int64_t)4 << 30) / 4;
+    int64_t warps = std::min<int64_t>((int64_t)h->sm_count * 4 * occupancy_blocks((const void*)traceback_kernel, 128, 0),
+                                      std::max<int64_t>(4, budget_words / std::max<int64_t>(dir_words, 1)));
+    warps = std::min<int64_t>(warps, std::max<int64_t>(4, n_pairs));
+    warps = (warps + 3) / 4 * 4;
+    {
+        sw_status_t e = ensure(h, h->tb_dir, (size_t)(warps * dir_words));
+        if (e != SW_OK) return e;
+        e = ensure(h, h->tb_bnd, (size_t)(warps * bnd_len));
+        if (e != SW_OK) return e;
+    }
+    TraceParams T;
+    T.queries = queries; T.q_off = q_offsets; T.refs = refs; T.r_off = r_offsets; T.n_pairs = n_pairs;
+    T.q0 = q0; T.r0 = r0; T.res = *res; T.ops = ops; T.n_ops = n_ops; T.sc = sc;
+    T.dir = h->tb_dir.p; T.dir_words = dir_words; T.bnd = h->tb_bnd.p; T.bnd_len = bnd_len;
+    T.counter = h->d_tb + 2; T.err = h->d_tb + 3;
+    traceback_kernel<<<(int)(warps / 4), 128, 0, s>>>(T);
+    SW_CUDA(h, cudaGetLastError());
+    h->last_stream = s;
+    return SW_OK;
+}
+
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
     if (mode != SW_MODE_FULL && mode != SW_MODE_END_ONLY) return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
@@ -850,6 +911,9 @@ sw_status_t sw_free(sw_handle_t h) {
     if (h->d_counters) cudaFree(h->d_counters);
     if (h->d_sink) cudaFree(h->d_sink);
     if (h->d_hist) cudaFree(h->d_hist);
+    if (h->d_tb) cudaFree(h->d_tb);
+    if (h->h_tb) cudaFreeHost(h->h_tb);
+    release(h->tb_dir); release(h->tb_bnd);
     if (h->d_binbase) cudaFree(h->d_binbase);
     for (auto& ev : h->ev) if (ev) cudaEventDestroy(ev);
     for (int k = 0; k < MAX_CHUNKS; ++k) {

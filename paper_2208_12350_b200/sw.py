@@ -32,7 +32,7 @@ SW_STAGE_NAMES = ("pack", "sort", "fwd", "mid", "rev", "finish")
 SW_MODE_FULL = 0
 SW_MODE_END_ONLY = 1
 
-EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_batch_status", "sw_free",
+EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
             "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_last_reverse_cells", "sw_dpx_peak")
 
@@ -81,6 +81,7 @@ def load(build_if_missing: bool = True):
     lib.sw_submit_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_wait.argtypes = [vp]
     lib.sw_set_mode.argtypes = [vp, ctypes.c_int32]
+    lib.sw_traceback.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp, vp, vp]
     lib.sw_batch_status.argtypes = [vp, ctypes.POINTER(i64)]
     lib.sw_free.argtypes = [vp]
     lib.sw_status_string.argtypes = [ctypes.c_int]
@@ -274,6 +275,44 @@ class Aligner:
         a, b = ctypes.c_int32(0), ctypes.c_int32(0)
         load().sw_last_launch_count(ctypes.c_void_p(self.handle), ctypes.byref(a), ctypes.byref(b))
         return a.value, b.value
+
+    def traceback_tensors(self, q, qo, r, ro, scoring: dict, res, ops=None, n_ops=None):
+        """Alignment ops of an aligned batch (include/sw.h sw_traceback); res = the (5, n) result
+        tensor of align_tensors.  Returns (ops uint8 tensor, n_ops int32 tensor), on the device."""
+        import torch
+        n = qo.numel() - 1
+        if ops is None:
+            ops = torch.empty(int(q.numel() + r.numel()) + 1, dtype=torch.uint8, device=q.device)
+        if n_ops is None:
+            n_ops = torch.empty(max(n, 1), dtype=torch.int32, device=q.device)
+        rr = sw_result_t(res[0].data_ptr(), res[1].data_ptr(), res[2].data_ptr(), res[3].data_ptr(), res[4].data_ptr())
+        st = load().sw_traceback(ctypes.c_void_p(self.handle), ctypes.c_void_p(q.data_ptr()), ctypes.c_void_p(qo.data_ptr()),
+                                 ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(ro.data_ptr()), int(n),
+                                 ctypes.byref(make_scoring(scoring)), ctypes.byref(rr), ctypes.c_void_p(ops.data_ptr()),
+                                 ctypes.c_void_p(n_ops.data_ptr()), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if st != SW_OK:
+            raise SWError(st, sw_last_error_message(self.handle))
+        return ops, n_ops
+
+    def traceback(self, batch) -> list:
+        """Align a host batch and return each pair's op string ('' for S == 0, None for invalid)."""
+        import torch
+        q, qo, r, ro = self.to_device(batch)
+        out, _ = self.align_tensors(q, qo, r, ro, batch.scoring)
+        ops, n_ops = self.traceback_tensors(q, qo, r, ro, batch.scoring, out)
+        torch.cuda.synchronize()
+        ops_h = ops.cpu().numpy().tobytes()
+        n_h = n_ops.cpu().numpy()
+        qoff, roff = batch.q_offsets, batch.r_offsets
+        res = []
+        for p in range(batch.n_pairs):
+            k = int(n_h[p])
+            if k < 0:
+                res.append(None)
+                continue
+            at = int(qoff[p] - qoff[0] + roff[p] - roff[0])
+            res.append(ops_h[at:at + k].decode())
+        return res
 
     def set_mode(self, mode: int):
         """SW_MODE_FULL (forward + reverse) or SW_MODE_END_ONLY (forward only; starts not written)."""

@@ -440,3 +440,54 @@ def test_end_only_mode(aligner):
     got = aligner.align(b)
     for f in FIELDS:
         np.testing.assert_array_equal(got[f], exp[f])
+
+
+# ------------------------------------------------------------ alignment paths (f1)
+
+def _oracle_paths(b: synth.Batch):
+    exp = oracle_batch(b)
+    out = []
+    for p in range(b.n_pairs):
+        q, r = b.pair(p)
+        res = tuple(int(exp[f][p]) for f in FIELDS)
+        out.append(oracle.traceback(q, r, b.scoring, res) if res[0] >= 0 else None)
+    return out
+
+
+@pytest.mark.parametrize("which", ["c1", "c2", "c3", "ties", "long", "edges"])
+def test_traceback_paths_match_oracle(aligner, which):
+    """sw_traceback: every pair's op string equal to the oracle's path (reading R20)."""
+    rng = np.random.default_rng(17)
+    if which == "c1":
+        b = synth.generate("c1")
+    elif which == "c2":
+        b = synth.generate("c2", 0, 1500)
+    elif which == "c3":
+        b = synth.generate("c3", 0, 300)
+    elif which == "ties":
+        pairs = [("".join(rng.choice(list("AC"), int(rng.integers(1, 40)))),
+                  "".join(rng.choice(list("AC"), int(rng.integers(1, 40))))) for _ in range(400)]
+        b = synth.from_pairs(pairs, {"alphabet": "dna", "match": 2, "mismatch": -2, "gap_open": -1, "gap_extend": -1})
+    elif which == "long":
+        # multi-stripe intervals (> 160 query rows) with indels
+        pairs = []
+        for k in range(40):
+            n = int(rng.integers(150, 700))
+            q = "".join(rng.choice(list("ACGT"), n))
+            mut = list(q)
+            for _ in range(n // 25):
+                pos = int(rng.integers(0, len(mut)))
+                if rng.random() < 0.5:
+                    del mut[pos]
+                else:
+                    mut.insert(pos, str(rng.choice(list("ACGT"))))
+            pairs.append((q, "".join(rng.choice(list("ACGT"), 30)) + "".join(mut)))
+        b = synth.from_pairs(pairs, synth.DNA_SCORING)
+    else:
+        pairs = [("", "ACGT"), ("ACGT", ""), ("A", "A"), ("A", "C"), ("ACNT", "ACGT"), ("ACGT", "ACGT" * 3),
+                 ("GGGGAAAAGGGG", "GGGGGGGG"), ("ACGTACGT", "ACGTTACGT")]
+        b = synth.from_pairs(pairs, synth.DNA_SCORING)
+    got = aligner.traceback(b)
+    exp = _oracle_paths(b)
+    bad = [p for p in range(b.n_pairs) if got[p] != exp[p]]
+    assert not bad, f"{len(bad)} paths differ; first pair {bad[0]}: gpu={got[bad[0]]!r} oracle={exp[bad[0]]!r}"
