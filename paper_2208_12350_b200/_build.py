@@ -12,7 +12,7 @@ LIB = os.path.join(PKG, "libsw_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["sw_api.cu"]
-HEADERS = ["sw_common.cuh", "sw_pack.cuh", "sw_wavefront.cuh", "sw_finish.cuh"]
+HEADERS = ["sw_common.cuh", "sw_pack.cuh", "sw_wavefront.cuh", "sw_finish.cuh", "sw_bin.cuh", "sw_traceback.cuh"]
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
