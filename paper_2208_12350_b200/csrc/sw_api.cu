@@ -753,7 +753,7 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
     const int64_t q0 = reinterpret_cast<int64_t*>(h->h_tb + 4)[0], r0 = reinterpret_cast<int64_t*>(h->h_tb + 4)[1];
     // 2. one warp per pair; the warp count is capped so the direction scratch stays <= 4 GiB
     const int64_t ns = std::max<int64_t>(1, ((int64_t)max_a + TB_ROWS - 1) / TB_ROWS);
-    const int64_t dir_words = ns * ((int64_t)max_b + 31) * 32;
+    const int64_t dir_words = ns * (((int64_t)max_b + 31 + 31) & ~(int64_t)31) * 32;
     const int64_t bnd_len = (int64_t)max_b + 1;
     const int64_t budget_words = ((int64_t)4 << 30) / 4;
     int64_t warps = std::min<int64_t>((int64_t)h->sm_count * 4 * occupancy_blocks((const void*)traceback_kernel, 128, 0),

@@ -10,7 +10,9 @@
 //      wavefront (32 lanes x 5 rows = 160-row stripes, int32 lanes), storing 5
 //      bits per cell -- H's preferred predecessor (diagonal / F / E, in that
 //      priority), F opened here, F extended here, E opened here -- as one
-//      32-bit word per lane and step (coalesced stores, step-major layout);
+//      32-bit word per lane and step, staged per 32 steps in shared memory and
+//      written lane-major (each lane one 128-byte line), so the walk below
+//      stays inside a line for up to 32 consecutive steps (L1 hits);
 //   2. one lane walks the path back from (a, b) through the stored bits with
 //      the state machine of oracle_traceback's definition (the bits of the
 //      cell above / to the left give the next op's preference in gap states);
@@ -61,6 +63,7 @@ __global__ void trace_extent_kernel(sw_result_t res, int64_t n_pairs, const int6
 
 __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
     __shared__ uint8_t lut[256];
+    __shared__ uint32_t tbuf[4][32][33];  // per warp: 32 steps x 32 lanes of direction words (padded)
     __shared__ int8_t s_sigma[24 * 24];
     for (int c = threadIdx.x; c < 256; c += blockDim.x) lut[c] = ascii_code(P.sc.alphabet, c);
     for (int k = threadIdx.x; k < 24 * 24; k += blockDim.x)
@@ -71,6 +74,7 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         return dna ? (a == b ? P.sc.match : P.sc.mismatch) : (int)s_sigma[a * 24 + b];
     };
     const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     uint32_t* dir = P.dir + gwarp * P.dir_words;
     int2* bnd = P.bnd + gwarp * P.bnd_len;
@@ -90,7 +94,8 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         const int a = qe - qs + 1, b = re - rs + 1;
         const int ns = (a + TB_ROWS - 1) / TB_ROWS;
         const int steps = b + 31;           // column j (1-based) of lane L at step t: j = t - L + 1
-        if ((int64_t)ns * steps * 32 > P.dir_words || b + 1 > P.bnd_len) {
+        const int steps_pad = (steps + 31) & ~31;
+        if ((int64_t)ns * steps_pad * 32 > P.dir_words || b + 1 > P.bnd_len) {
             if (lane == 0) { P.n_ops[p] = -1; atomicAdd(P.err, 1); }
             continue;
         }
@@ -146,7 +151,16 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
                     if (lane == 31) bnd[j] = make_int2(hoLast, fLast);  // for the next stripe
                 }
                 diagUp = upH;
-                dir[((int64_t)s * steps + t) * 32 + lane] = word;
+                tbuf[wib][lane][t & 31] = word;
+                if ((t & 31) == 31 || t == steps - 1) {  // flush 32 steps: lane L writes its own line
+                    __syncwarp();
+                    uint32_t* dst = dir + ((int64_t)(s * 32 + lane) * steps_pad + (t & ~31));
+#pragma unroll
+                    for (int k = 0; k < 32; k += 4)
+                        *reinterpret_cast<uint4*>(dst + k) =
+                            make_uint4(tbuf[wib][lane][k], tbuf[wib][lane][k + 1], tbuf[wib][lane][k + 2], tbuf[wib][lane][k + 3]);
+                    __syncwarp();
+                }
             }
             __syncwarp();
             if (lane == 31) bnd[0] = make_int2(o + (s + 1) * TB_ROWS * e - e, 0);  // H[row0 of next stripe - 1][0]
@@ -161,7 +175,7 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
             auto bits = [&](int i, int j) -> uint32_t {  // 1-based interior cell
                 const int s = (i - 1) / TB_ROWS, L = ((i - 1) % TB_ROWS) / TB_K, r = (i - 1) % TB_K;
                 const int t = j - 1 + L;
-                return (dir[((int64_t)s * steps + t) * 32 + L] >> (5 * r)) & 31u;
+                return (dir[(int64_t)(s * 32 + L) * steps_pad + t] >> (5 * r)) & 31u;
             };
             // H's preferred move at (i, j): 0 diagonal, 1 F, 2 E (border cells: no diagonal; H == F on column 0)
             auto pref = [&](int i, int j) -> int {

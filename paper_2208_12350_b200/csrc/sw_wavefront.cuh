@@ -48,7 +48,15 @@
 #define SW_MIN_BLOCKS 4
 #endif
 #ifndef SW_BODY_BLOCKS
-#define SW_BODY_BLOCKS 1   // 4-column blocks per unrolled loop body (forward)
+#define SW_BODY_BLOCKS 2   // 4-column blocks per unrolled loop body (forward; chosen by tools/gevo_search.py)
+#endif
+// Launch bounds of the 8-row (protein) geometry: 3-warp blocks, 5 per SM by shared memory, so
+// up to 136 registers per thread keep all 15 warps resident.
+#ifndef SW_PROT_THREADS
+#define SW_PROT_THREADS 96
+#endif
+#ifndef SW_PROT_BLOCKS
+#define SW_PROT_BLOCKS 5
 #endif
 #ifndef SW_CODE_DIST
 #define SW_CODE_DIST 4     // reference-code prefetch distance in columns
@@ -272,6 +280,9 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 
     // rotating prefetch of the next U columns' codes (and boundary rows)
     constexpr int CD = SW_CODE_DIST < U ? SW_CODE_DIST : U;  // code prefetch distance (columns)
+    // the prefetch ring is indexed u % CD within a U-column block: CD must divide U (a distance of 3
+    // with U = 4 reads wrong codes -- the variant search's parity gate rejected it)
+    static_assert(U % CD == 0, "SW_CODE_DIST must divide the column unroll");
     uint32_t cd[CD][NH];
     uint2 bnd[U];
 #pragma unroll
@@ -469,7 +480,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 }
 
 template <class T, int W, int K, bool REV, bool TAG>
-__global__ void __launch_bounds__(128, SW_MIN_BLOCKS) wavefront_kernel(const WaveParams P) {
+__global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
+    wavefront_kernel(const WaveParams P) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
