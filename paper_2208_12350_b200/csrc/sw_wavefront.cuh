@@ -50,6 +50,9 @@
 #ifndef SW_BODY_BLOCKS
 #define SW_BODY_BLOCKS 2   // 4-column blocks per unrolled loop body (forward; chosen by tools/gevo_search.py)
 #endif
+#ifndef SW_REV_BODY_BLOCKS
+#define SW_REV_BODY_BLOCKS 1  // reverse pass: the stop column is re-checked after every block either way
+#endif
 // Launch bounds of the 8-row (protein) geometry: 3-warp blocks, 5 per SM by shared memory, so
 // up to 136 registers per thread keep all 15 warps resident.
 #ifndef SW_PROT_THREADS
@@ -330,7 +333,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     }
     // NB blocks of U columns per loop iteration (the longer body lets ptxas keep loop-carried
     // values in place); tag bookkeeping stays per U-column block
-    constexpr int NB = REV ? 1 : SW_BODY_BLOCKS;
+    constexpr int NB = REV ? SW_REV_BODY_BLOCKS : SW_BODY_BLOCKS;
     int t00 = 0;
     for (; t00 < T_end; t00 += U * NB) {
 #pragma unroll
