@@ -430,6 +430,12 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "stage_ms": {k: round(v, 4) for k, v in stage_med.items()},
         "swept_over_real_cells": round(swept / max(fwd_cells, 1), 4),
         "status": {"batch_status": sw.status_string(st), "bad_pairs": nbad},
+        # the paper reports kernel runtimes of ADEPT (one block per pair) on pre-Hopper GPUs, no GCUPS
+        # (BASELINE.md sec. 1): quoted as context, not comparable targets
+        "paper_numbers": {"ADEPT-V0 -> GEVO, 30k DNA pairs, int16": {"P100": "2362 ms -> 72 ms", "GTX 1080Ti":
+                          "1442 ms -> 45 ms", "V100": "918 ms -> 50 ms"},
+                          "ADEPT-V1 GEVO speedup": {"P100": 1.28, "GTX 1080Ti": 1.31, "V100": 1.17},
+                          "source": "PAPER.md:297-298 (BASELINE.md sec. 1)"},
     }
     if cpu:
         line["cpu_baseline"] = cpu
