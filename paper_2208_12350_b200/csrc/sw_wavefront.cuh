@@ -50,6 +50,9 @@
 #ifndef SW_BODY_BLOCKS
 #define SW_BODY_BLOCKS 2   // 4-column blocks per unrolled loop body (forward; chosen by tools/gevo_search.py)
 #endif
+#ifndef SW_SKEW2
+#define SW_SKEW2 0         // 1: forward TAG sweep with a two-column skew per lane (sweep_skew2; measured slower)
+#endif
 #ifndef SW_REV_BODY_BLOCKS
 #define SW_REV_BODY_BLOCKS 1  // reverse pass: the stop column is re-checked after every block either way
 #endif
@@ -482,6 +485,152 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     return t00;  // column steps swept (statistics)
 }
 
+// Forward TAG sweep with a two-column skew per lane (single stripe, no end events): lane L's
+// upper rows 0..4 work on column t - 2L while its lower rows 5..9 work on column t - 2L - 1.
+// The lower rows need this lane's row 4 from the previous step and the row above (the previous
+// lane's row 9) arrives from the previous step as before, so within a step the two 5-row chains
+// are independent: half the dependent-chain length per column step for the same instruction
+// count, at the price of W more fill/drain steps.  The tag of a cell orders lower rows before
+// upper rows of the same step (their column is one smaller), so the block maximum still names
+// the lexmin (j, i) cell (reading R5).
+template <class T, int W, int K>
+__device__ __forceinline__ int sweep_skew2(const WaveParams& P, const uint8_t* prof, const int seg, const int L,
+                                           const int (&h_pid)[T::NH], const int64_t (&h_rpos)[T::NH], const int mmax,
+                                           const int row0, const uint32_t o2, const uint32_t e2, const int o) {
+    using G = Geometry<W, K, T>;
+    constexpr int NH = T::NH;
+    static_assert(NH == 2 && K == 10 && G::PWORDS == 4, "two-column skew: s16x2, 10 rows per lane");
+    constexpr int KU = 5;                 // upper rows 0..4, lower rows 5..9
+    constexpr int U = 4;                  // column steps per tag block
+    constexpr int NB = SW_BODY_BLOCKS;
+    constexpr int CS = W * G::PB;
+    constexpr int CD = SW_CODE_DIST < U ? SW_CODE_DIST : U;
+    static_assert(U % CD == 0, "SW_CODE_DIST must divide the column unroll");
+    constexpr uint32_t TAGSET = 0x003f003fu;
+    constexpr uint32_t SEL[4] = {0xC480u, 0xD591u, 0xE6A2u, 0xF7B3u};
+    const int nc = P.sc.nc;
+
+    Quads<K> HO;
+    uint32_t E[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) { HO[r] = 0u; E[r] = 0u; }
+    const uint32_t floor2 = T::splat(-o);
+    const uint32_t one = P.one;
+    uint32_t best = TAGSET;
+    int brow[NH], bc[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) { brow[h] = 0; bc[h] = 0; }
+    uint32_t prof_h[NH];
+    const uint8_t* rp[NH];
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        prof_h[h] = (uint32_t)__cvta_generic_to_shared(prof + (size_t)(seg * NH + h) * nc * CS + (size_t)L * G::PB);
+        rp[h] = P.rcode + h_rpos[h] - 2 * L;  // this lane's upper column 0 (pad codes before it)
+    }
+    const uint32_t cs = opaque(CS);
+    const uint32_t notL0 = opaque(L != 0 ? 1u : 0u);
+    uint32_t hoLast = 0u, fLast = 0u, prevUpHO = 0u;  // lower row 9 (previous step); row above's diagonal
+    uint32_t f4 = 0u, ho4pp = 0u;                     // row 4's F (previous step), row 4's H two steps back
+    uint32_t pwl[NH][2];                              // previous step's profile words 1, 2 (rows 4..11)
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {                    // step 0's lower column is a pad column
+        const uint4 v = lds128(prof_h[h] + (uint32_t)(nc - 1) * cs);
+        pwl[h][0] = v.y; pwl[h][1] = v.z;
+    }
+    uint32_t cd[CD][NH];
+#pragma unroll
+    for (int u = 0; u < CD; ++u)
+#pragma unroll
+        for (int h = 0; h < NH; ++h) cd[u][h] = ld_code(rp[h] + u);
+
+    // decode a block maximum v (one half): column and row of its cell
+    auto decode = [&](int v, int t0, int& col, int& row) {
+        const int step = t0 + (U - 1 - ((v >> 4) & 3));
+        const int rho = 15 - (v & 15);
+        if (rho < KU) { row = rho + KU; col = step - 2 * L - 1; }
+        else { row = rho - KU; col = step - 2 * L; }
+    };
+    auto tag_commit = [&](uint32_t nbt, int t0) {
+        const uint32_t d = nbt ^ best;
+#pragma unroll
+        for (int h = 0; h < NH; ++h)
+            if ((d >> (16 * h)) & 0xffffu) decode(T::get(nbt, h), t0, bc[h], brow[h]);
+        best = nbt | TAGSET;
+    };
+
+    const int T_end = mmax + 2 * W - 1;
+    int t00 = 0;
+    for (; t00 < T_end; t00 += U * NB) {
+#pragma unroll
+        for (int bb = 0; bb < NB; ++bb) {
+            const int t0 = t00 + bb * U;
+            uint32_t nbt = best;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + u;
+                uint32_t pw[NH][4];
+#pragma unroll
+                for (int h = 0; h < NH; ++h) {
+                    const uint4 v = lds128(prof_h[h] + cd[u % CD][h] * cs);
+                    pw[h][0] = v.x; pw[h][1] = v.y; pw[h][2] = v.z; pw[h][3] = v.w;
+                    cd[u % CD][h] = ld_code(rp[h] + t + CD);
+                }
+                const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0;
+                const uint32_t upF = __shfl_up_sync(FULL, fLast, 1, W) * notL0;
+                uint32_t H[K];
+                // lower rows 5..9, column t - 2L - 1 (profile words of the previous step)
+                {
+                    uint32_t hd = ho4pp, hu = HO[4], F = f4;
+#pragma unroll
+                    for (int r = KU; r < K; ++r) {
+                        const uint32_t sc = prmt(pwl[0][(r >> 2) - 1], pwl[NH - 1][(r >> 2) - 1], SEL[r & 3]);
+                        E[r] = T::addmax(E[r], e2, HO[r]);
+                        F = T::addmax(F, e2, hu);
+                        const uint32_t tt = T::max3(E[r], F, floor2);
+                        const uint32_t hb = T::addmax(hd, sc, tt);
+                        hd = HO[r];
+                        HO[r] = hb * one + o2;
+                        hu = HO[r];
+                        H[r] = HO[r] * P.tag_mul + (uint32_t)((U - 1 - u) * 16 + 15 - (r - KU)) * 0x10001u;
+                    }
+                    hoLast = HO[K - 1];
+                    fLast = F;
+                }
+                ho4pp = HO[4];
+                // upper rows 0..4, column t - 2L
+                {
+                    uint32_t hd = prevUpHO, hu = upHO, F = upF;
+                    prevUpHO = upHO;
+#pragma unroll
+                    for (int r = 0; r < KU; ++r) {
+                        const uint32_t sc = prmt(pw[0][r >> 2], pw[NH - 1][r >> 2], SEL[r & 3]);
+                        E[r] = T::addmax(E[r], e2, HO[r]);
+                        F = T::addmax(F, e2, hu);
+                        const uint32_t tt = T::max3(E[r], F, floor2);
+                        const uint32_t hb = T::addmax(hd, sc, tt);
+                        hd = HO[r];
+                        HO[r] = hb * one + o2;
+                        hu = HO[r];
+                        H[r] = HO[r] * P.tag_mul + (uint32_t)((U - 1 - u) * 16 + 15 - (r + KU)) * 0x10001u;
+                    }
+                    f4 = F;
+                }
+#pragma unroll
+                for (int h = 0; h < NH; ++h) { pwl[h][0] = pw[h][1]; pwl[h][1] = pw[h][2]; }
+#pragma unroll
+                for (int r = 0; r + 1 < K; r += 2) nbt = T::max3(nbt, H[r], H[r + 1]);
+            }
+            if (nbt != best) tag_commit(nbt, t0);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < NH; ++h) {
+        const int b = T::get(best, h) >> 6;
+        if (h_pid[h] >= 0 && b > 0) atomicMax(P.keys + h_pid[h], pack_key(b, bc[h], row0 + L * K + brow[h]));
+    }
+    return t00;
+}
+
 template <class T, int W, int K, bool REV, bool TAG>
 __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
     wavefront_kernel(const WaveParams P) {
@@ -644,7 +793,15 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             __syncwarp();
 
             // ---- the stripe's column sweep (single-stripe items skip all hand-off code) ----
-            if (SW_SINGLE_ONLY || ns == 1) {
+            bool swept = false;
+            if constexpr (SW_SKEW2 && TAGF && !REV && K == 10 && NH == 2 && G::PWORDS == 4) {
+                if (!need_ev && ns == 1) {
+                    steps += sweep_skew2<T, W, K>(P, prof, seg, L, h_pid, h_rpos, mmax, row0, o2, e2, o);
+                    swept = true;
+                }
+            }
+            if (swept) {
+            } else if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
                     steps += sweep<T, W, K, REV, false, true, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
