@@ -1,20 +1,22 @@
 // sw_wavefront.cuh -- steps a3 (forward: score + end) and a4 (reverse: start)
 // of SURVEY.md sec. 8(a): the anti-diagonal Gotoh wavefront on sm_100a.
 //
-// Recurrence (affine state PAPER.md:507/713-714).  The
-// kernel keeps E and F shifted by -o (o = gap_open < 0) and H both plain and
-// shifted, so every value stays >= 0 and the "+ o" step is a plain 32-bit add
-// (IMAD on the FMA pipe: no borrow crosses the 16-bit halves) instead of a
-// DPX add on the integer ALU pipe:
-//   Eb[i][j] = max(Eb[i][j-1] + e, H[i][j-1])                 VIADDMNMX
-//   Fb[i][j] = max(Fb[i-1][j] + e, H[i-1][j])                 VIADDMNMX
-//   t        = max(Eb, Fb, -o)                                VIMNMX3
-//   Hb[i][j] = max(H[i-1][j-1] + (s(q_i, r_j) - o), t)        VIADDMNMX
-//   H[i][j]  = Hb[i][j] + o                                   IMAD
-// with Eb = E - o, Fb = F - o, Hb = H - o; this is the plain recurrence
-// H = max(H[i-1][j-1] + s, E, F, 0), E = max(E[i][j-1] + e, H[i][j-1] + o),
-// F = max(F[i-1][j] + e, H[i-1][j] + o), with E/F relu-clamped at o and the
-// -inf borders replaced by gap_open (pin P13, reading R13).
+// Recurrence (affine state PAPER.md:507/713-714), in the
+// clamped form the kernel runs (SW_XFORM, default).  With E^ = max(E, 0),
+// F^ = max(F, 0), X = max(H[i-1][j-1] + s, E^) and R = H + o (o = gap_open):
+//   E^[i][j] = max(E^[i][j-1] + e, R[i][j-1], 0)             VIADDMNMX.RELU
+//   X[i][j]  = max(R[i-1][j-1] + (s - o), E^[i][j])          VIADDMNMX
+//   F^[i][j] = max(F^[i-1][j] + e, X[i-1][j] + o, 0)         VIADDMNMX.RELU
+//   R[i][j]  = max(F^[i][j] + o, X[i][j] + o)                VIADDMNMX (X + o: VIADD.16x2, FMA pipe)
+// which is H = max(H[i-1][j-1] + s, E, F, 0), E = max(E[i][j-1] + e, H[i][j-1] + o),
+// F = max(F[i-1][j] + e, H[i-1][j] + o) with E, F clamped at 0 (exact: e <= 0
+// and o <= e, pin P13, readings R13/R21).  F^ of the next row needs
+// only X + o of this one (H + o = max(X + o, F^ + o) and F^ + o <= F^ + e), so
+// the dependency chain down a lane's rows is ONE operation per row; E^ and X
+// depend only on the previous column.  The running max tracks X: an H = F^ > X
+// lies strictly below an X of a row above, so max X = S and the cells holding S
+// are the cells with X = S.  SW_XFORM=0 keeps the previous shifted-state update
+// (E, F, H kept minus o; four dependent operations per row).
 //
 // Layout (B200-first, not ADEPT's block-per-pair / thread-per-residue):
 // * a warp is split into 32/W segments of W lanes; a segment owns one (s32)
@@ -49,6 +51,12 @@
 #endif
 #ifndef SW_BODY_BLOCKS
 #define SW_BODY_BLOCKS 2   // 4-column blocks per unrolled loop body (forward; chosen by tools/gevo_search.py)
+#endif
+#ifndef SW_XFORM
+#define SW_XFORM 1         // clamped-E/F cell update with a one-op row chain (see sweep<>); 0: shifted-state update
+#endif
+#ifndef SW_TAG_LAZY
+#define SW_TAG_LAZY 1      // TAG forward: branch-free block commit, column/row decode deferred to emit
 #endif
 #ifndef SW_SKEW2
 #define SW_SKEW2 0         // 1: forward TAG sweep with a two-column skew per lane (sweep_skew2; measured slower)
@@ -171,6 +179,14 @@ __device__ __forceinline__ void sv_store(uint32_t addr, const Quads<K>& HO) {
                      "r"(K % 4 == 1 ? HO.q[K / 4].x : HO.q[K / 4].z) : "memory");
 }
 
+template <int K>
+__device__ __forceinline__ void sv_store_arr(uint32_t addr, const uint32_t (&v)[K]) {
+    Quads<K> q;
+#pragma unroll
+    for (int r = 0; r < K; ++r) q[r] = v[r];
+    sv_store<K>(addr, q);
+}
+
 // First row r of the saved column whose half h equals `target` (an HO value).
 template <class T, int K>
 __device__ __forceinline__ int sv_first_row(uint32_t addr, int h, int target) {
@@ -222,7 +238,11 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     Quads<K> HO;   // H of the lane's rows at the previous column (plain, >= 0)
     uint32_t E[K]; // Eb = E - o of the lane's rows at the previous column (>= 0)
 #pragma unroll
-    for (int r = 0; r < K; ++r) { HO[r] = 0u; E[r] = 0u; }
+    const uint32_t o2s = T::splat(o);      // gap_open in every half
+    // XF: HO holds R = H + o (column -1: H = 0), E holds max(E, 0); else HO holds H, E holds E - o
+    const uint32_t R0 = SW_XFORM ? o2s : 0u;
+#pragma unroll
+    for (int r = 0; r < K; ++r) { HO[r] = R0; E[r] = 0u; }
     const uint32_t floor2 = T::splat(-o);  // Hb floor: H >= 0  <=>  Hb >= -o
     const uint32_t one = P.one;
     // TAG: the running max holds H*64 + (3 - u)*16 + (15 - r) for the cell of row r in the
@@ -238,6 +258,10 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     uint32_t best = TAG ? TAGSET : 0u;
     int brow[NH];                        // TAG: row of the half's last improvement
     int bc[NH];                          // column of the last strict improvement, per half
+    // TAG (lazy commit): block start column and raw block maximum of the half's last improving
+    // block; decoded into bc / brow only when the half emits
+    int bt0[NH];
+    uint32_t btag[NH];
     uint32_t sv[NH];                     // shared address of the half's saved column
     int ev[NH];
     int next_ev = 0x7fffffff;
@@ -245,11 +269,13 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     for (int h = 0; h < NH; ++h) {
         bc[h] = 0;
         brow[h] = 0;
+        bt0[h] = 0;
+        btag[h] = 0u;
         sv[h] = sv_base + (uint32_t)h * G::SVB;
         ev[h] = (EV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
         next_ev = min(next_ev, ev[h]);
     }
-    uint32_t hoLast = 0u, fLast = 0u, prevUpHO = 0u;
+    uint32_t hoLast = R0, fLast = 0u, prevUpHO = R0;
     uint32_t prof_h[NH];  // shared-window address of this lane's profile entries, code 0
     const uint8_t* rp[NH];
 #pragma unroll
@@ -260,11 +286,21 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     const uint32_t cs = opaque(CS);  // code stride as a runtime value: the address is one IMAD
     // lane 0 takes the row above from the stripe boundary: up = shfl * notL0 + b (IMAD)
     const uint32_t notL0 = opaque(L != 0 ? 1u : 0u);
-    // (H = 0, F = o above row 0: H = 0, Fb = 0)
-    const uint32_t b0 = 0u;
+    // lane 0's row above at the top of the query (H = 0, F = -inf clamped): XF (R = o, F = 0),
+    // else (H = 0, Fb = 0); other lanes add 0 to the shuffled value
+    const uint32_t b0 = (SW_XFORM && L == 0) ? o2s : 0u;
 
     auto emit = [&](int h) {  // forward result of half h for this lane and stripe
         const int b = TAG ? (T::get(best, h) >> 6) : T::get(best, h);
+        if (TAG && SW_TAG_LAZY) {
+            uint32_t t0s, raw;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t0s), "=r"(raw) : "r"(sv[h]) : "memory");
+            bt0[h] = (int)t0s;
+            btag[h] = raw;
+            const int v = T::get(btag[h], h);
+            bc[h] = bt0[h] + (U - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
+            brow[h] = ((1 << RB) - 1) - (v & ((1 << RB) - 1));
+        }
         if (h_pid[h] >= 0 && b > 0) {
             const int rr = TAG ? brow[h] : sv_first_row<T, K>(sv[h], h, b);
             atomicMax(P.keys + h_pid[h], pack_key(b, bc[h], row0 + L * K + rr));
@@ -273,6 +309,17 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     // TAG: fold the block's running max into the per-half records (block start column t0)
     auto tag_commit = [&](uint32_t nbt, int t0) {
         const uint32_t d = nbt ^ best;
+        if (SW_TAG_LAZY) {
+            // branch-free: two compares and predicated moves (FMA-pipe IMAD.MOV); the decode of
+            // column and row from the raw maximum waits for emit()
+            // per half: record (block start, raw maximum) in the half's shared slot when it changed
+            // (predicated STS on the LSU pipe instead of SELs on the saturated ALU pipe)
+            asm volatile("{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %3, 0;\n\tsetp.ge.u32 q, %4, 65536;\n\t"
+                         "@p st.shared.v2.u32 [%0], {%2, %5};\n\t@q st.shared.v2.u32 [%1], {%2, %5};\n\t}"
+                         :: "r"(sv[0]), "r"(sv[NH - 1]), "r"(t0), "r"(d << 16), "r"(d), "r"(nbt) : "memory");
+            best = nbt | TAGSET;
+            return;
+        }
 #pragma unroll
         for (int h = 0; h < NH; ++h) {
             if ((d >> (16 * h)) & 0xffffu) {
@@ -296,7 +343,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 #pragma unroll
         for (int h = 0; h < NH; ++h)
             if (u < CD) cd[u][h] = ld_code(rp[h] + u);
-        if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, b0);
+        if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, 0u);
     }
 
     // reverse pass: packed targets of both halves (the forward score S of each pair); the
@@ -365,12 +412,12 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 }
                 cd[u % CD][h] = ld_code(rp[h] + t + CD);
             }
-            uint32_t bHO = b0, bF = b0;
+            uint32_t bHO = b0, bF = 0u;
             if (MULTI) {
                 bHO = bnd[u].x; bF = bnd[u].y;
                 // columns past the item's longest reference were never handed off: they take
                 // the constant boundary, so pad-column cells stay below S (see EV above)
-                bnd[u] = (from_scratch && L == 0 && t + U < mmax) ? __ldcg(scr_in + t + U) : make_uint2(b0, b0);
+                bnd[u] = (from_scratch && L == 0 && t + U < mmax) ? __ldcg(scr_in + t + U) : make_uint2(b0, 0u);
             }
             // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
             const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
@@ -378,7 +425,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             uint32_t hd = prevUpHO;
             prevUpHO = upHO;
             uint32_t F = upF, hu = upHO;
-            uint32_t H[K];
+            uint32_t H[K];  // per row: the value the running max tracks (XF: X, else H), TAG-tagged
 #pragma unroll
             for (int r = 0; r < K; ++r) {
                 uint32_t sc;
@@ -390,15 +437,36 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 } else {
                     sc = pw[0][r];
                 }
-                E[r] = T::addmax(E[r], e2, HO[r]);          // Eb[i][j] = max(Eb[i][j-1] + e, H[i][j-1])
-                F = T::addmax(F, e2, hu);                   // Fb[i][j] = max(Fb[i-1][j] + e, H[i-1][j])
-                const uint32_t tt = T::max3(E[r], F, floor2);  // max(E, F, 0) - o
-                const uint32_t hb = T::addmax(hd, sc, tt);  // max(H[i-1][j-1] + s, E, F, 0) - o
-                hd = HO[r];
-                HO[r] = hb * one + o2;                      // H = Hb + o: one IMAD, no borrow (Hb >= -o)
-                hu = HO[r];
-                // TAG: H*64 + tag per half, one IMAD on the FMA pipe (H <= 511: no carry)
-                H[r] = TAG ? HO[r] * P.tag_mul + (uint32_t)((U - 1 - u) * (1 << RB) + (1 << RB) - 1 - r) * 0x10001u : HO[r];
+                uint32_t xv;
+                if (SW_XFORM) {
+                    // E^ = max(E, 0), F^ = max(F, 0), X = max(H[i-1][j-1] + s, E^) (>= 0), R = H + o:
+                    //   E^[i][j] = max(E^[i][j-1] + e, R[i][j-1], 0)          VIADDMNMX.RELU
+                    //   X[i][j]  = max(R[i-1][j-1] + (s - o), E^[i][j])       VIADDMNMX
+                    //   F^[i][j] = max(F^[i-1][j] + e, X[i-1][j] + o, 0)      VIADDMNMX.RELU (the row chain)
+                    //   R[i][j]  = max(F^[i][j] + o, X[i][j] + o)             VIADDMNMX (+ VIADD.16x2, FMA pipe)
+                    // H = max(X, F^); F^ feeds F^ of the next row through X + o only (o <= e), so the
+                    // dependency chain down a lane's rows is one operation per row.  The running max
+                    // tracks X: every H = F^ > X lies strictly below some X of a row above, so max X = S
+                    // and the cells with H = S are exactly those with X = S.
+                    E[r] = T::addmax_relu(E[r], e2, HO[r]);
+                    xv = T::addmax(hd, sc, E[r]);
+                    F = T::addmax_relu(F, e2, hu);
+                    const uint32_t xo = T::add(xv, o2s);
+                    hd = HO[r];
+                    HO[r] = T::addmax(F, o2s, xo);
+                    hu = xo;
+                } else {
+                    E[r] = T::addmax(E[r], e2, HO[r]);          // Eb[i][j] = max(Eb[i][j-1] + e, H[i][j-1])
+                    F = T::addmax(F, e2, hu);                   // Fb[i][j] = max(Fb[i-1][j] + e, H[i-1][j])
+                    const uint32_t tt = T::max3(E[r], F, floor2);  // max(E, F, 0) - o
+                    const uint32_t hb = T::addmax(hd, sc, tt);  // max(H[i-1][j-1] + s, E, F, 0) - o
+                    hd = HO[r];
+                    HO[r] = hb * one + o2;                      // H = Hb + o: one IMAD, no borrow (Hb >= -o)
+                    hu = HO[r];
+                    xv = HO[r];
+                }
+                // TAG: value*64 + tag per half, one IMAD on the FMA pipe (value <= 511: no carry)
+                H[r] = TAG ? xv * P.tag_mul + (uint32_t)((U - 1 - u) * (1 << RB) + (1 << RB) - 1 - r) * 0x10001u : xv;
             }
             hoLast = HO[K - 1];
             fLast = F;
@@ -422,7 +490,12 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                             if (((x >> (16 * h)) & (NH == 1 ? 0xffffffffu : 0xffffu)) == 0u && h_pid[h] >= 0) {
                                 int rr = 0;
 #pragma unroll
-                                for (int r = K - 1; r >= 0; --r) if (T::get(H[r], h) == h_tgt[h]) rr = r;
+                                // whole-word compare under the half's mask (no 16-bit extraction, which
+                                // makes ptxas split the row values into 16-bit pieces in the hot path)
+                                const uint32_t tw = T::splat(h_tgt[h]);
+                                const uint32_t msk = NH == 1 ? 0xffffffffu : (h ? 0xffff0000u : 0x0000ffffu);
+#pragma unroll
+                                for (int r = K - 1; r >= 0; --r) if (((H[r] ^ tw) & msk) == 0u) rr = r;
                                 atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
                                 atomicMin((int*)stop + seg * NH + h, t - L + W);
                                 tgt2 = T::set(tgt2, h, -1);
@@ -438,7 +511,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     for (int h = 0; h < NH; ++h) {
                         if (NH == 1 || ((d >> (16 * h)) & 0xffffu)) {
                             bc[h] = t - L;
-                            sv_store<K>(sv[h], HO);
+                            if (SW_XFORM) sv_store_arr<K>(sv[h], H); else sv_store<K>(sv[h], HO);
                         }
                     }
                     best = nb;
@@ -463,7 +536,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
             }
         }
-        if (TAG && !REV && nbt != best) tag_commit(nbt, t0);
+        if (TAG && !REV && (SW_TAG_LAZY || nbt != best)) tag_commit(nbt, t0);
         if (TAG && REV) {
             const uint32_t x = T::max2(nbt, tgt64) ^ nbt;  // zero half: block max >= S*64
             if (((x - 0x00010001u) & ~x & 0x80008000u) != 0u) rev_tag_find(nbt, t0);

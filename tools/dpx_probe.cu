@@ -10,6 +10,10 @@
 #define CHAINS 8
 #define ITERS 4096
 
+__device__ __forceinline__ unsigned hmax2(unsigned a, unsigned b) {
+    unsigned d; asm volatile("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b)); return d;
+}
+
 struct Out { unsigned long long cycles; unsigned v; };
 
 __device__ __forceinline__ unsigned prmt(unsigned a, unsigned b, unsigned s) {
@@ -29,7 +33,7 @@ __device__ __forceinline__ unsigned prmt(unsigned a, unsigned b, unsigned s) {
 template <int V>
 __global__ void probe(Out* out, unsigned seed, unsigned o2, unsigned e2) {
     unsigned h[CHAINS], e[CHAINS], f[CHAINS], x[CHAINS];
-    unsigned best = 0;
+    unsigned best = 0, tgp = 0;
 #pragma unroll
     for (int c = 0; c < CHAINS; ++c) {
         h[c] = seed * (c + 1) + threadIdx.x; e[c] = h[c] ^ 0x5555; f[c] = h[c] + 77; x[c] = h[c] * 3;
@@ -94,6 +98,25 @@ __global__ void probe(Out* out, unsigned seed, unsigned o2, unsigned e2) {
                 x[c] = h[c];
                 h[c] = __vadd2(H, o2);
                 if (c & 1) best = __vimax3_s16x2_relu(best, H, h[c - 1]);
+            } else if (V == 15) {
+                h[c] = hmax2(h[c], e[c]);
+                e[c] = e[c] * seed + f[c];
+            } else if (V == 16) {
+                h[c] = __viaddmax_s16x2(h[c], e2, e[c]);
+                x[c] = hmax2(x[c], h[c]);
+            } else if (V == 17 || V == 18) {
+                // the shipped TAG cell (E, F addmax; max3; H addmax; PRMT; HO and tag IMADs) with the
+                // running max by VIMNMX3 (0.5 per cell pair, V17) or by max.f16x2 (1 per cell pair, V18)
+                unsigned sc = prmt(x[c], s, 0x3210 + (c & 3));
+                e[c] = __viaddmax_s16x2(e[c], e2, h[c]);
+                f[c] = __viaddmax_s16x2(f[c], e2, h[c]);
+                unsigned t = __vimax3_s16x2(e[c], f[c], e2);
+                unsigned hb = __viaddmax_s16x2(x[c], sc, t);
+                x[c] = h[c];
+                h[c] = hb * seed + o2;
+                unsigned tg = h[c] * 64u + (unsigned)c * 0x10001u;
+                if (V == 17) { if (c & 1) best = __vimax3_s16x2(best, tg, tgp); else tgp = tg; }
+                else best = hmax2(best, tg);
             } else if (V == 14) {
                 h[c] = __viaddmax_s16x2(h[c], e2, e[c]);
                 x[c] = (x[c] != f[c]) ? x[c] : e[c];
@@ -112,10 +135,11 @@ __global__ void probe(Out* out, unsigned seed, unsigned o2, unsigned e2) {
 }
 
 // instructions per chain-iteration (per thread) that the probe is meant to measure
-static const double INSTR_PER_CHAIN[15] = {5.5, 1, 1, 1, 1, 6.5, 5.5, 2, 2, 1, 1, 2, 6.5, 5.5, 3};
-static const char* NAMES[15] = {"mix5.5(s16x2 gotoh)", "VIADDMNMX.S16x2", "VIMNMX3.S16x2(+LOP)", "PRMT", "IMAD",
+static const double INSTR_PER_CHAIN[19] = {5.5, 1, 1, 1, 1, 6.5, 5.5, 2, 2, 1, 1, 2, 6.5, 5.5, 3, 2, 2, 8.5, 8};
+static const char* NAMES[19] = {"mix5.5(s16x2 gotoh)", "VIADDMNMX.S16x2", "VIMNMX3.S16x2(+LOP)", "PRMT", "IMAD",
                                 "mix+PRMT(6.5)", "mix,IMAD for H+o", "VIADDMNMX+IMAD", "LOP3 x2", "SHFL",
-                                "VIADD.16x2", "VIADDMNMX+VIADD.16x2", "cell v2 +PRMT (6.5)", "cell v2 (5.5)", "VIADDMNMX+ISETP+SEL"};
+                                "VIADD.16x2", "VIADDMNMX+VIADD.16x2", "cell v2 +PRMT (6.5)", "cell v2 (5.5)", "VIADDMNMX+ISETP+SEL",
+                                "HMNMX2+IMAD", "VIADDMNMX+HMNMX2", "TAG cell, max3 best", "TAG cell, f16x2 best"};
 
 template <int V>
 void run(int sms, int blocks_per_sm, int threads) {
@@ -138,7 +162,7 @@ void run(int sms, int blocks_per_sm, int threads) {
     double mhz = (cyc / (ms * 1e-3)) / 1e6;
     printf("%-22s warps/SM=%2d  warp-instr/clk/SM=%.3f  GPU warp-instr/s=%.3e  implied SM MHz=%.0f  ms=%.3f\n",
            NAMES[V], warps_per_sm, ipc, wall_rate, mhz, ms);
-    if (V == 0 || V == 5 || V == 6 || V == 12 || V == 13) {
+    if (V == 0 || V == 5 || V == 6 || V == 12 || V == 13 || V == 17 || V == 18) {
         double cellpairs = (double)CHAINS * ITERS * 32.0 * warps;
         printf("    -> cell updates/s (2 cells per s16x2 chain step) = %.3f TCUPS\n", 2 * cellpairs / (ms * 1e-3) / 1e12);
     }
@@ -155,6 +179,7 @@ int main() {
         run<4>(sms, bps, 256); run<5>(sms, bps, 256); run<6>(sms, bps, 256); run<7>(sms, bps, 256);
         run<8>(sms, bps, 256); run<9>(sms, bps, 256); run<10>(sms, bps, 256); run<11>(sms, bps, 256);
         run<12>(sms, bps, 256); run<13>(sms, bps, 256); run<14>(sms, bps, 256);
+        run<15>(sms, bps, 256); run<16>(sms, bps, 256); run<17>(sms, bps, 256); run<18>(sms, bps, 256);
     }
     return 0;
 }
