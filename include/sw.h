@@ -91,10 +91,14 @@ typedef struct {
  * mode): SW_MODE_FULL (default) runs the forward and the
  * reverse pass; SW_MODE_END_ONLY runs the forward pass only -- score, q_end
  * and r_end are exact as in FULL mode, q_start / r_start are not written (the
- * sw_result_t pointers may then be NULL).  Applies to every later call on
- * the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown mode.
+ * sw_result_t pointers may then be NULL).  Flag SW_MODE_AFFINE_ONLY (may be
+ * OR-ed with either) keeps linear-gap scorings (gap_open == gap_extend) on the
+ * affine kernels instead of the two-state linear-gap kernels (PAPER.md:161-163:
+ * the gap scores are free parameters; results are identical either way -- the
+ * flag exists for comparison and testing).  Applies to every later call on
+ * the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown mode bit.
  */
-typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1 } sw_mode_t;
+typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2 } sw_mode_t;
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
 
 /*

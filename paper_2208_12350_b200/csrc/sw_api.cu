@@ -34,12 +34,28 @@ namespace {
 constexpr int W16 = SW_W16, K16 = SW_K16;
 // protein: 8 rows per lane keep the 25-code int8 profile at 8 bytes per (code, lane) -> 12.8 KB per
 // warp, so shared memory allows 16 resident warps per SM (10 rows would need 16-byte entries)
-constexpr int WP = 16, KP = 8;
+#ifndef SW_KP
+#define SW_KP 8
+#endif
+constexpr int WP = 16, KP = SW_KP;
 constexpr int W32 = 16, K32 = 10;
 constexpr int WARPS_PER_BLOCK = 4;
 using G16 = Geometry<W16, K16, TS16>;
 using GP = Geometry<WP, KP, TS16>;
 using G32 = Geometry<W32, K32, TS32>;
+
+// The wavefront kernel of a pass (REV), gap model (LIN: gap_open == gap_extend), alphabet and
+// route.  The int32 route keeps the affine kernel for linear gaps (same results, o = e).
+template <bool REV, bool LIN>
+const void* wave_kernel_ptr(bool protein, int route) {
+    if (route == ROUTE_S32) return (const void*)wavefront_kernel<TS32, W32, K32, REV, false, false>;
+    const bool tag = route == ROUTE_TAG;
+    if (protein)
+        return tag ? (const void*)wavefront_kernel<TS16, WP, KP, REV, true, LIN>
+                   : (const void*)wavefront_kernel<TS16, WP, KP, REV, false, LIN>;
+    return tag ? (const void*)wavefront_kernel<TS16, W16, K16, REV, true, LIN>
+               : (const void*)wavefront_kernel<TS16, W16, K16, REV, false, LIN>;
+}
 
 template <class T>
 struct DevBuf {
@@ -321,7 +337,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     int32_t* counters = h->d_counters + slot * 8;
     h->ev_valid = false;
     if (n_pairs == 0) return SW_OK;
-    const bool end_only = h->mode == SW_MODE_END_ONLY;
+    const bool end_only = (h->mode & SW_MODE_END_ONLY) != 0;
     if (!queries || !q_off || !refs || !r_off || !out || !out->score || !out->q_end || !out->r_end ||
         (!end_only && (!out->q_start || !out->r_start)))
         return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
@@ -405,16 +421,14 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[2], s));
 
     // one kernel per route and pass (routes: TAG, S16, S32; sw_common.cuh)
-    const void* kfwd[N_ROUTES] = {protein ? (const void*)wavefront_kernel<TS16, WP, KP, false, true>
-                                          : (const void*)wavefront_kernel<TS16, W16, K16, false, true>,
-                                  protein ? (const void*)wavefront_kernel<TS16, WP, KP, false, false>
-                                          : (const void*)wavefront_kernel<TS16, W16, K16, false, false>,
-                                  (const void*)wavefront_kernel<TS32, W32, K32, false, false>};
-    const void* krev[N_ROUTES] = {protein ? (const void*)wavefront_kernel<TS16, WP, KP, true, true>
-                                          : (const void*)wavefront_kernel<TS16, W16, K16, true, true>,
-                                  protein ? (const void*)wavefront_kernel<TS16, WP, KP, true, false>
-                                          : (const void*)wavefront_kernel<TS16, W16, K16, true, false>,
-                                  (const void*)wavefront_kernel<TS32, W32, K32, true, false>};
+    // linear gaps (gap_open == gap_extend) take the two-state kernels of the s16x2 routes
+    const bool lin = sc.gap_open == sc.gap_extend && !(h->mode & SW_MODE_AFFINE_ONLY);
+    const void* kfwd[N_ROUTES];
+    const void* krev[N_ROUTES];
+    for (int r = 0; r < N_ROUTES; ++r) {
+        kfwd[r] = lin ? wave_kernel_ptr<false, true>(protein, r) : wave_kernel_ptr<false, false>(protein, r);
+        krev[r] = lin ? wave_kernel_ptr<true, true>(protein, r) : wave_kernel_ptr<true, false>(protein, r);
+    }
     Launch lf[N_ROUTES], lr[N_ROUTES];
     for (int r = 0; r < N_ROUTES; ++r) {
         // reverse-pass pairs are a subset of the forward ones (finish_fwd may move TAG pairs to
@@ -565,16 +579,13 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
     h->sm_count = p.multiProcessorCount;
     // opt in to large dynamic shared memory (protein profiles)
     const int big = 200 * 1024;
-    set_smem_attr(wavefront_kernel<TS16, WP, KP, false, true>, big);
-    set_smem_attr(wavefront_kernel<TS16, WP, KP, true, true>, big);
-    set_smem_attr(wavefront_kernel<TS16, WP, KP, false, false>, big);
-    set_smem_attr(wavefront_kernel<TS16, WP, KP, true, false>, big);
-    set_smem_attr(wavefront_kernel<TS16, W16, K16, false, true>, big);
-    set_smem_attr(wavefront_kernel<TS16, W16, K16, true, true>, big);
-    set_smem_attr(wavefront_kernel<TS16, W16, K16, false, false>, big);
-    set_smem_attr(wavefront_kernel<TS16, W16, K16, true, false>, big);
-    set_smem_attr(wavefront_kernel<TS32, W32, K32, false, false>, big);
-    set_smem_attr(wavefront_kernel<TS32, W32, K32, true, false>, big);
+    for (int pr = 0; pr < 2; ++pr)
+        for (int r = 0; r < N_ROUTES; ++r) {
+            set_smem_attr(wave_kernel_ptr<false, false>(pr, r), big);
+            set_smem_attr(wave_kernel_ptr<true, false>(pr, r), big);
+            set_smem_attr(wave_kernel_ptr<false, true>(pr, r), big);
+            set_smem_attr(wave_kernel_ptr<true, true>(pr, r), big);
+        }
     set_smem_attr(bin_scan_kernel, BIN_SCAN_SMEM);
     if (cudaMalloc(&h->d_stats, N_SLOTS * sizeof(BatchStats)) != cudaSuccess ||
         cudaMallocHost(&h->h_stats, N_SLOTS * sizeof(BatchStats)) != cudaSuccess ||
@@ -713,7 +724,7 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
         if (st != SW_OK) { result = st; break; }
         SW_CUDA(h, cudaEventRecord(h->ev_out[k], cs));
         SW_CUDA(h, cudaStreamWaitEvent(h->copy_stream, h->ev_out[k], 0));
-        for (int f = 0; f < (h->mode == SW_MODE_END_ONLY ? 3 : 5); ++f)
+        for (int f = 0; f < ((h->mode & SW_MODE_END_ONLY) ? 3 : 5); ++f)
             if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f] + a, h->st_out.p + f * N + a, (size_t)(b - a) * 4,
                                                    cudaMemcpyDeviceToHost, h->copy_stream));
     }
@@ -779,7 +790,7 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
 
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
-    if (mode != SW_MODE_FULL && mode != SW_MODE_END_ONLY) return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
+    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY)) return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
     h->mode = mode;
     return SW_OK;
 }
@@ -858,7 +869,7 @@ sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t*
     // results out on their own stream (the copy-in stream keeps feeding the next batch)
     SW_CUDA(h, cudaStreamWaitEvent(h->out_stream, h->as_comp[k], 0));
     int32_t* dst[5] = {out_host->score, out_host->q_end, out_host->r_end, out_host->q_start, out_host->r_start};
-    for (int f = 0; f < (h->mode == SW_MODE_END_ONLY ? 3 : 5); ++f)
+    for (int f = 0; f < ((h->mode & SW_MODE_END_ONLY) ? 3 : 5); ++f)
         if (dst[f]) SW_CUDA(h, cudaMemcpyAsync(dst[f], o + f * N, N * 4, cudaMemcpyDeviceToHost, h->out_stream));
     SW_CUDA(h, cudaEventRecord(h->as_done[k], h->out_stream));
     h->as_used[k] = true;

@@ -55,6 +55,12 @@
 #ifndef SW_XFORM
 #define SW_XFORM 1         // clamped-E/F cell update with a one-op row chain (see sweep<>); 0: shifted-state update
 #endif
+#ifndef SW_PROT_T4
+#define SW_PROT_T4 1       // protein profile build from a transposed (s - o) table with byte transposes
+#endif
+#ifndef SW_T4_ALL
+#define SW_T4_ALL 0
+#endif
 #ifndef SW_TAG_LAZY
 #define SW_TAG_LAZY 1      // TAG forward: branch-free block commit, column/row decode deferred to emit
 #endif
@@ -222,7 +228,7 @@ __device__ __forceinline__ uint4 lds_rem(uint32_t addr) {
 // every half emits after the sweep, which is exact when the item's
 // references differ by at most the pad margin (the columns past a shorter
 // reference are pad codes, whose cells stay below S).
-template <class T, int W, int K, bool REV, bool MULTI, bool EV, bool TAG>
+template <class T, int W, int K, bool REV, bool MULTI, bool EV, bool TAG, bool LIN>
 __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const uint32_t sv_base,
                                       const int seg, const int L, const int s_m, const int (&h_pid)[T::NH],
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
@@ -421,7 +427,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             }
             // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
             const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
-            const uint32_t upF = __shfl_up_sync(FULL, fLast, 1, W) * notL0 + bF;
+            const uint32_t upF = LIN ? 0u : __shfl_up_sync(FULL, fLast, 1, W) * notL0 + bF;
             uint32_t hd = prevUpHO;
             prevUpHO = upHO;
             uint32_t F = upF, hu = upHO;
@@ -438,7 +444,18 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     sc = pw[0][r];
                 }
                 uint32_t xv;
-                if (SW_XFORM) {
+                if (LIN) {
+                    // linear gaps (gap_open == gap_extend = e): with R = H + e,
+                    //   A[i][j] = max(R[i-1][j-1] + (s - e), R[i][j-1], 0)     VIADDMNMX.RELU
+                    //   H[i][j] = max(A[i][j], R[i-1][j])                      VIMNMX
+                    //   R[i][j] = H[i][j] + e                                  VIADD.16x2 (FMA pipe)
+                    // (the affine recurrence with o = e: E[i][j] = H[i][j-1] + e since E <= H).
+                    // The running max tracks A: H = R[i-1][j] > A lies below a larger H (e < 0).
+                    xv = T::addmax_relu(hd, sc, HO[r]);
+                    hd = HO[r];
+                    HO[r] = T::add(T::max2(xv, hu), o2s);
+                    hu = HO[r];
+                } else if (SW_XFORM) {
                     // E^ = max(E, 0), F^ = max(F, 0), X = max(H[i-1][j-1] + s, E^) (>= 0), R = H + o:
                     //   E^[i][j] = max(E^[i][j-1] + e, R[i][j-1], 0)          VIADDMNMX.RELU
                     //   X[i][j]  = max(R[i-1][j-1] + (s - o), E^[i][j])       VIADDMNMX
@@ -704,7 +721,7 @@ __device__ __forceinline__ int sweep_skew2(const WaveParams& P, const uint8_t* p
     return t00;
 }
 
-template <class T, int W, int K, bool REV, bool TAG>
+template <class T, int W, int K, bool REV, bool TAG, bool LIN>
 __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
     wavefront_kernel(const WaveParams P) {
     using G = Geometry<W, K, T>;
@@ -718,9 +735,26 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
     // substitution table for the profile builds, in shared memory: lanes index it with
     // divergent codes, which a constant-bank table would serialise
     __shared__ int8_t s_sigma[24 * 24];
+    // protein s16x2 profiles: (s - o) bytes of query residue a against codes 4q..4q+3 in word
+    // s_t4[a][q]; row a = 24 is the pad residue (-128 against every code), code 24 the pad code
+    constexpr int TQ = (NC_PROTEIN + 3) / 4;
+    __shared__ uint32_t s_t4[SW_T4_ALL || K == 8 ? 25 * TQ : 1];  // K == 8: the protein geometry
     for (int k = threadIdx.x; k < 24 * 24; k += blockDim.x) {
         const int a = k / 24, b = k % 24;
         s_sigma[k] = (int8_t)(P.sc.alphabet == SW_ALPHABET_DNA ? 0 : c_blosum62[a][b]);
+    }
+    if (NH == 2 && (SW_T4_ALL || K == 8) && P.sc.alphabet != SW_ALPHABET_DNA) {
+        for (int k = threadIdx.x; k < 25 * TQ; k += blockDim.x) {
+            const int a = k / TQ, q = k % TQ;
+            uint32_t word = 0u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int c = 4 * q + b;
+                const int v = (a < 24 && c < 24) ? c_blosum62[a][c] - P.sc.gap_open : -128;
+                word |= (uint32_t)(v & 0xff) << (8 * b);
+            }
+            s_t4[k] = word;
+        }
     }
     __syncthreads();
     auto sigma = [&](int a, int b) -> int {
@@ -833,6 +867,30 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
                             *reinterpret_cast<uint32_t*>(base + (size_t)c * W * G::PB) = word;
                         }
                         *reinterpret_cast<uint32_t*>(base + (size_t)(nc - 1) * W * G::PB) = padw;
+                    } else if (NH == 2 && SW_PROT_T4 && (SW_T4_ALL || K == 8)) {
+                        // protein: four rows' residues index the transposed table; a 4x4 byte
+                        // transpose (8 PRMT) turns four table words into the words of four codes
+                        uint32_t qa[4];
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int r = w * 4 + b;
+                            const int i = row0 + l * K + r;
+                            qa[b] = (pid >= 0 && r < K && i < n) ? (uint32_t)P.qcode[REV ? qp + n - 1 - i : qp + i] * TQ
+                                                                 : 24u * TQ;
+                        }
+#pragma unroll
+                        for (int q = 0; q < TQ; ++q) {
+                            const uint32_t w0 = s_t4[qa[0] + q], w1 = s_t4[qa[1] + q];
+                            const uint32_t w2 = s_t4[qa[2] + q], w3 = s_t4[qa[3] + q];
+                            const uint32_t t0 = prmt(w0, w1, 0x5140u), t1 = prmt(w0, w1, 0x7362u);
+                            const uint32_t t2 = prmt(w2, w3, 0x5140u), t3 = prmt(w2, w3, 0x7362u);
+                            const uint32_t ow[4] = {prmt(t0, t2, 0x5410u), prmt(t0, t2, 0x7632u),
+                                                    prmt(t1, t3, 0x5410u), prmt(t1, t3, 0x7632u)};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (4 * q + k < NC_PROTEIN)
+                                    *reinterpret_cast<uint32_t*>(base + (size_t)(4 * q + k) * W * G::PB) = ow[k];
+                        }
                     } else if (NH == 2) {
                         int qc[4];
 #pragma unroll
@@ -876,10 +934,10 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             if (swept) {
             } else if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, false, true, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
                 else
-                    steps += sweep<T, W, K, REV, false, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                       row0, o2, e2, o, nullptr, nullptr, false, false);
             } else {
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
@@ -887,10 +945,10 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
                 uint2* scr_out = reinterpret_cast<uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, true, true, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
                 else
-                    steps += sweep<T, W, K, REV, true, false, TAGF>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
             }
         }

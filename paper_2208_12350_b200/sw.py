@@ -31,6 +31,7 @@ SW_MAX_SEQ_LEN = 65535
 SW_STAGE_NAMES = ("pack", "sort", "fwd", "mid", "rev", "finish")
 SW_MODE_FULL = 0
 SW_MODE_END_ONLY = 1
+SW_MODE_AFFINE_ONLY = 2
 
 EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
@@ -315,7 +316,8 @@ class Aligner:
         return res
 
     def set_mode(self, mode: int):
-        """SW_MODE_FULL (forward + reverse) or SW_MODE_END_ONLY (forward only; starts not written)."""
+        """SW_MODE_FULL (forward + reverse) or SW_MODE_END_ONLY (forward only; starts not written),
+        optionally OR-ed with SW_MODE_AFFINE_ONLY (linear-gap scorings stay on the affine kernels)."""
         st = load().sw_set_mode(ctypes.c_void_p(self.handle), int(mode))
         if st != SW_OK:
             raise SWError(st, sw_last_error_message(self.handle))

@@ -491,3 +491,45 @@ def test_traceback_paths_match_oracle(aligner, which):
     exp = _oracle_paths(b)
     bad = [p for p in range(b.n_pairs) if got[p] != exp[p]]
     assert not bad, f"{len(bad)} paths differ; first pair {bad[0]}: gpu={got[bad[0]]!r} oracle={exp[bad[0]]!r}"
+
+
+# ------------------------------------------------------------ linear gaps (f2)
+
+def _rescored(b: synth.Batch, sc: dict) -> synth.Batch:
+    import dataclasses
+    return dataclasses.replace(b, scoring=dict(sc))
+
+
+@pytest.mark.parametrize("which", ["dna_tag", "dna_s16_stripes", "protein", "ties"])
+def test_linear_gap_kernels(aligner, which):
+    """gap_open == gap_extend takes the two-state linear-gap kernels: all five
+    fields equal to the oracle (affine recurrence with o = e) and to the affine kernels
+    (SW_MODE_AFFINE_ONLY) on the same bytes."""
+    rng = np.random.default_rng(31)
+    if which == "dna_tag":       # 150-row reads, max_s * n <= 511: TAG route
+        b = _rescored(synth.generate("c2", 0, 1500),
+                      {"alphabet": "dna", "match": 2, "mismatch": -3, "gap_open": -2, "gap_extend": -2})
+    elif which == "dna_s16_stripes":   # long queries: S16 route, several stripes, lane/stripe edges
+        pairs = []
+        for n in (1, 10, 159, 160, 161, 321, 700, 1300):
+            for m in (1, 17, 300, 900):
+                q = "".join(rng.choice(list("ACGT"), n))
+                s0 = int(rng.integers(0, max(1, n - 5)))
+                r = ("".join(rng.choice(list("ACGT"), m // 3)) + q[s0:s0 + m])[:m]
+                pairs.append((q, r))
+        b = synth.from_pairs(pairs, {"alphabet": "dna", "match": 3, "mismatch": -2, "gap_open": -3, "gap_extend": -3})
+    elif which == "protein":
+        b = _rescored(synth.generate("c3", 0, 600),
+                      {"alphabet": "protein", "match": 0, "mismatch": 0, "gap_open": -4, "gap_extend": -4})
+    else:
+        pairs = [("AC" * L, "CA" * (L + 3)) for L in (1, 5, 16, 80, 200)]
+        pairs += [("".join(rng.choice(list("AC"), L)), "".join(rng.choice(list("AC"), L + 9))) for L in (7, 60, 170, 400)]
+        b = synth.from_pairs(pairs, {"alphabet": "dna", "match": 1, "mismatch": -1, "gap_open": -1, "gap_extend": -1})
+    got = run_and_compare(aligner, b)
+    aligner.set_mode(sw.SW_MODE_AFFINE_ONLY)
+    try:
+        aff = aligner.align(b)
+    finally:
+        aligner.set_mode(sw.SW_MODE_FULL)
+    for f in FIELDS:
+        np.testing.assert_array_equal(got[f], aff[f])
