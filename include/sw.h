@@ -155,6 +155,26 @@ sw_status_t sw_align_batch(sw_handle_t h,
                            const sw_result_t* out, void* stream);
 
 /*
+ * One query against a database of references (the
+ * paper's problem statement, with A fixed): results are
+ * those of sw_align_batch on the pairs (query, refs[r_offsets[p] ..
+ * r_offsets[p+1])), p = 0 .. n_refs - 1, q coordinates relative to the query.
+ *   query             DEVICE uint8 ASCII, n bytes (n >= 0)
+ *   refs, r_offsets,
+ *   n_refs, scoring,
+ *   out, stream       as for sw_align_batch (n_refs pairs)
+ * The query is broadcast on `stream` into a handle-owned device buffer of
+ * n * n_refs bytes (the batch path then packs and profiles it like any other
+ * query).  Errors as for sw_align_batch; SW_ERR_INVALID_ARGUMENT for n < 0 or
+ * a NULL query with n > 0.
+ */
+sw_status_t sw_align_query_db(sw_handle_t h,
+                              const uint8_t* query, int64_t n,
+                              const uint8_t* refs, const int64_t* r_offsets,
+                              int64_t n_refs, const sw_scoring_t* scoring,
+                              const sw_result_t* out, void* stream);
+
+/*
  * Same computation with HOST buffers (pinned memory recommended): copies the
  * inputs to handle-owned device staging buffers, aligns, and copies the five
  * result arrays to the HOST pointers in `out_host`.  Synchronous: returns

@@ -110,6 +110,8 @@ struct sw_context {
     DevBuf<uint8_t> as_q[2], as_r[2];
     DevBuf<int64_t> as_qo[2], as_ro[2];
     DevBuf<int32_t> as_out[2];
+    DevBuf<uint8_t> db_q;     // sw_align_query_db: the broadcast query
+    DevBuf<int64_t> db_qo;
     cudaEvent_t as_in[2] = {}, as_comp[2] = {}, as_done[2] = {}, as_start = nullptr;
     bool as_used[2] = {false, false};
     bool as_inflight = false;
@@ -626,6 +628,46 @@ sw_status_t sw_align_batch(sw_handle_t h, const uint8_t* queries, const int64_t*
                            const sw_result_t* out, void* stream) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
     return align_impl(h, queries, q_offsets, refs, r_offsets, n_pairs, scoring, out, (cudaStream_t)stream, nullptr);
+}
+
+namespace {
+// sw_align_query_db: q[p * n + i] = query[i], qo[p] = p * n (16-byte stores when n is a multiple of 16)
+__global__ void broadcast_query_kernel(const uint8_t* __restrict__ query, int64_t n, int64_t n_refs,
+                                       uint8_t* __restrict__ q, int64_t* __restrict__ qo) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t p = tid; p <= n_refs; p += stride) qo[p] = p * n;
+    if ((n & 15) == 0 && (((uintptr_t)query) & 15) == 0) {
+        const int64_t nv = n >> 4, total = nv * n_refs;
+        for (int64_t k = tid; k < total; k += stride)
+            reinterpret_cast<uint4*>(q)[k] = __ldg(reinterpret_cast<const uint4*>(query) + k % nv);
+    } else {
+        const int64_t total = n * n_refs;
+        for (int64_t k = tid; k < total; k += stride) q[k] = query[k % n];
+    }
+}
+}  // namespace
+
+sw_status_t sw_align_query_db(sw_handle_t h, const uint8_t* query, int64_t n, const uint8_t* refs,
+                              const int64_t* r_offsets, int64_t n_refs, const sw_scoring_t* scoring,
+                              const sw_result_t* out, void* stream) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (n < 0 || (n > 0 && !query)) return fail(h, SW_ERR_INVALID_ARGUMENT, "query: n < 0 or NULL pointer");
+    if (n_refs < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "n_refs < 0");
+    if (n_refs == 0) return SW_OK;
+    int dev = -1;
+    SW_CUDA(h, cudaGetDevice(&dev));
+    if (dev != h->device) return fail(h, SW_ERR_WRONG_DEVICE, "current device differs from the handle's device");
+    cudaStream_t s = (cudaStream_t)stream;
+    sw_status_t st = ensure(h, h->db_q, (size_t)std::max<int64_t>(n * n_refs, 16));
+    if (st != SW_OK) return st;
+    st = ensure(h, h->db_qo, (size_t)n_refs + 1);
+    if (st != SW_OK) return st;
+    const int64_t work = std::max<int64_t>(n_refs + 1, n * n_refs / 16);
+    const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)h->sm_count * 8);
+    broadcast_query_kernel<<<blocks, 256, 0, s>>>(query, n, n_refs, h->db_q.p, h->db_qo.p);
+    SW_CUDA(h, cudaGetLastError());
+    return align_impl(h, h->db_q.p, h->db_qo.p, refs, r_offsets, n_refs, scoring, out, s, nullptr);
 }
 
 sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int64_t* q_offsets, const uint8_t* refs,

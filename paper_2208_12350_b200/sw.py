@@ -33,7 +33,7 @@ SW_MODE_FULL = 0
 SW_MODE_END_ONLY = 1
 SW_MODE_AFFINE_ONLY = 2
 
-EXPORTED = ("sw_init", "sw_align_batch", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
+EXPORTED = ("sw_init", "sw_align_batch", "sw_align_query_db", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
             "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_last_reverse_cells", "sw_dpx_peak")
 
@@ -79,6 +79,7 @@ def load(build_if_missing: bool = True):
     lib.sw_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
     lib.sw_align_batch.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_align_batch_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
+    lib.sw_align_query_db.argtypes = [vp, vp, i64, vp, vp, i64, sp, rp, vp]
     lib.sw_submit_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_wait.argtypes = [vp]
     lib.sw_set_mode.argtypes = [vp, ctypes.c_int32]
@@ -256,6 +257,32 @@ class Aligner:
         out, st = self.align_tensors(q, qo, r, ro, batch.scoring, check=check)
         self.torch.cuda.synchronize(self.device)
         n = batch.n_pairs
+        o = out[:, :n].cpu().numpy()
+        return {k: o[i] for i, k in enumerate(("score", "q_end", "r_end", "q_start", "r_start"))}
+
+    def align_query_db(self, query: bytes, refs, scoring: dict) -> dict:
+        """One query against a list of references (include/sw.h sw_align_query_db); returns the
+        five int32 numpy arrays, one entry per reference."""
+        t = self.torch
+        dev = f"cuda:{self.device}"
+        rb = [x.encode() if isinstance(x, str) else bytes(x) for x in refs]
+        ro = np.zeros(len(rb) + 1, dtype=np.int64)
+        ro[1:] = np.cumsum([len(x) for x in rb]) if rb else []
+        ra = np.frombuffer(b"".join(rb), dtype=np.uint8) if rb else np.zeros(0, np.uint8)
+        qa = np.frombuffer(bytes(query), dtype=np.uint8)
+        qd = t.from_numpy(qa.copy()).to(dev) if qa.size else t.zeros(1, dtype=t.uint8, device=dev)
+        rd = t.from_numpy(ra.copy()).to(dev) if ra.size else t.zeros(1, dtype=t.uint8, device=dev)
+        rod = t.from_numpy(ro).to(dev)
+        n = len(rb)
+        out = self.alloc_out(n)
+        res = sw_result_t(*[out[i].data_ptr() for i in range(5)])
+        st = load().sw_align_query_db(ctypes.c_void_p(self.handle), ctypes.c_void_p(qd.data_ptr()), int(qa.size),
+                                      ctypes.c_void_p(rd.data_ptr()), ctypes.c_void_p(rod.data_ptr()), n,
+                                      ctypes.byref(make_scoring(scoring)), ctypes.byref(res),
+                                      ctypes.c_void_p(t.cuda.current_stream(self.device).cuda_stream))
+        if st != SW_OK:
+            raise SWError(st, sw_last_error_message(self.handle))
+        t.cuda.synchronize(self.device)
         o = out[:, :n].cpu().numpy()
         return {k: o[i] for i, k in enumerate(("score", "q_end", "r_end", "q_start", "r_start"))}
 

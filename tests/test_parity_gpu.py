@@ -533,3 +533,18 @@ def test_linear_gap_kernels(aligner, which):
         aligner.set_mode(sw.SW_MODE_FULL)
     for f in FIELDS:
         np.testing.assert_array_equal(got[f], aff[f])
+
+
+# ------------------------------------------------------------ one query vs a database (f2)
+
+@pytest.mark.parametrize("alpha", ["dna", "protein"])
+def test_query_db_mode(aligner, alpha):
+    """sw_align_query_db: one query against many references equals the oracle on the pairs
+    (query, ref_p), including empty references and a query length that is not a multiple of 16."""
+    src = synth.generate("c2" if alpha == "dna" else "c3", 0, 400)
+    q, _ = src.pair(7)
+    refs = [src.pair(p)[1] for p in range(400)] + [b"", q, q[::-1]]
+    for query in (q, q[:37], b""):
+        b = synth.from_pairs([(query, r) for r in refs], src.scoring)
+        got = aligner.align_query_db(query, refs, src.scoring)
+        assert_parity(got, oracle_batch(b), b)
