@@ -11,7 +11,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libsw_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["sw_api.cu"]
+SOURCES = ["sw_api.cu", "simcov_diffuse.cu"]
 HEADERS = ["sw_common.cuh", "sw_pack.cuh", "sw_wavefront.cuh", "sw_finish.cuh", "sw_bin.cuh", "sw_traceback.cuh"]
 
 NVCC_FLAGS = [
@@ -27,7 +27,7 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "sw.h"), __file__]
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, h) for h in ("sw.h", "simcov.h")] + [__file__]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

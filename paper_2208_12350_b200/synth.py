@@ -240,3 +240,41 @@ def random_pairs(seed: int, count: int, n_range, m_range, alphabet: bytes = b"AC
         pairs.append((alpha[rng.integers(0, alpha.size, size=n)].tobytes(),
                       alpha[rng.integers(0, alpha.size, size=m)].tobytes()))
     return from_pairs(pairs, scoring or DNA_SCORING, name)
+
+
+# ------------------------------------------------------------ SIMCoV diffusion fields (f4)
+
+SIMCOV_HELDOUT = (2500, 2500)  # the held-out grid of PAPER.md:567 ("a larger grid size: 2500x2500")
+
+
+def simcov_fields(seed: int, H: int, W: int, n_fields: int = 2, sites: int | None = None,
+                  peak: int = 1 << 24, background: float = 0.0):
+    """Seeded SIMCoV-shaped concentration fields (uint32 H x W arrays, one per field).
+
+    SIMCoV seeds a lung-tissue grid with "a set of infection sites" from which virions and
+    inflammatory signal spread: each field is zero except at ``sites``
+    random points (default: one per 10,000 cells, at least 1) holding a concentration drawn
+    uniformly from [peak/2, peak), plus, if ``background`` > 0, that fraction of cells
+    holding a uniform value below peak/64 (an established, already-spread infection).
+    No diffusion arithmetic here: the same arrays go to the oracle and the CUDA path.
+    """
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([SEED_BASE, 22, seed])))
+    cells = H * W
+    k = max(1, cells // 10000) if sites is None else sites
+    out = []
+    for _ in range(n_fields):
+        f = np.zeros(cells, np.uint32)
+        if cells:
+            if background > 0:
+                nb = int(cells * background)
+                f[rng.integers(0, cells, size=nb)] = rng.integers(0, max(1, peak // 64), size=nb, dtype=np.uint32)
+            f[rng.integers(0, cells, size=min(k, cells))] = rng.integers(peak // 2, peak, size=min(k, cells),
+                                                                         dtype=np.uint32)
+        out.append(f.reshape(H, W))
+    return out
+
+
+def simcov_dense(seed: int, H: int, W: int, n_fields: int = 2, high: int = 1 << 31):
+    """Seeded uniform fields in [0, high) (tests: full-range arithmetic, every cell active)."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([SEED_BASE, 23, seed])))
+    return [rng.integers(0, high, size=(H, W), dtype=np.uint64).astype(np.uint32) for _ in range(n_fields)]

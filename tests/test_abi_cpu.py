@@ -74,3 +74,37 @@ def test_init_without_gpu_fails_cleanly():
     st = sw.load().sw_init(ctypes.byref(h), 0)
     assert st in (sw.SW_ERR_CUDA, sw.SW_ERR_INVALID_ARGUMENT)
     assert not h.value
+
+
+def simcov_declared():
+    text = open(os.path.join(ROOT, "include", "simcov.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(simcov_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_simcov_symbol():
+    from paper_2208_12350_b200 import simcov
+    lib = ctypes.CDLL(_build.build())
+    missing = [s for s in simcov_declared() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(simcov_declared()) == set(simcov.EXPORTED)
+
+
+def test_simcov_host_helpers():
+    """Padded layout (include/simcov.h): rows on 128 B, >= 4 zero words left, room for the
+    right neighbour of the last 128-column strip; no device needed."""
+    from paper_2208_12350_b200 import simcov
+    for W in (0, 1, 5, 120, 127, 128, 129, 2500, 16384):
+        p = simcov.simcov_grid_pitch(W)
+        strips = -(-W // 128) * 128
+        assert p % 32 == 0 and p >= strips + 8 and p - (strips + 8) < 32
+        assert simcov.simcov_grid_words(7, W) == 9 * p
+    assert simcov.simcov_grid_pitch(-1) == -1 and simcov.simcov_grid_words(-1, 3) == -1
+    with pytest.raises(sw.SWError):
+        simcov.simcov_set_schedule(simcov.SIMCOV_MAX_TBLOCK + 1)
+    simcov.simcov_set_schedule(0)
+    # argument errors are returned before anything touches a device
+    with pytest.raises(sw.SWError):
+        simcov.simcov_diffuse(None, None, 4, 4, 1, 4096, [0], 1)
+    with pytest.raises(sw.SWError):
+        simcov.simcov_diffuse(1 << 20, 2 << 20, 4, 4, 0, 4096, [0], 1)
