@@ -98,7 +98,7 @@ sw_status_t simcov_diffuse(uint32_t* grid, uint32_t* scratch, int64_t H, int64_t
  *   0 = auto (default), 1 = one step per launch, k >= 2 = up to k steps per
  *   launch through shared memory (temporal blocking), k <= SIMCOV_MAX_TBLOCK.
  * Errors: SW_ERR_INVALID_ARGUMENT for k outside [0, SIMCOV_MAX_TBLOCK]. */
-#define SIMCOV_MAX_TBLOCK 4
+#define SIMCOV_MAX_TBLOCK 8
 sw_status_t simcov_set_schedule(int32_t steps_per_launch);
 
 /* Number of kernels the last simcov_diffuse call of this thread enqueued. */

@@ -41,12 +41,18 @@ int32_t g_schedule = 0;
 
 constexpr int64_t kColPad = 4;   // interior starts at word 4 of a padded row
 constexpr int kStripCols = 128;  // one warp: 32 lanes x 4 cells
-constexpr int kTbMaxK = 4;       // temporal blocking: halo of 4 words covers k <= 4
-constexpr int kTbWarps = 8;
-constexpr int kTbRowsPerWarp = 9;
-constexpr int kTbRows = kTbWarps * kTbRowsPerWarp;  // 72 staged rows
-constexpr int kTbCols = 128;                        // staged words per row (32 lanes x 4)
-constexpr int kTbOutCols = kTbCols - 2 * 4;         // 120 written columns
+#ifndef SIMCOV_TB_WARPS
+#define SIMCOV_TB_WARPS 8
+#endif
+#ifndef SIMCOV_TB_RPW
+#define SIMCOV_TB_RPW 16
+#endif
+#ifndef SIMCOV_TB_KMAX
+#define SIMCOV_TB_KMAX 6
+#endif
+constexpr int kTbMaxK = SIMCOV_TB_KMAX;  // default steps per launch (halo 4 words for k <= 4, else 8)
+constexpr int kTbWarps = SIMCOV_TB_WARPS;
+constexpr int kTbRowsPerWarp = SIMCOV_TB_RPW;
 
 struct Rates {
     uint32_t a[SIMCOV_MAX_FIELDS];
@@ -133,81 +139,98 @@ __global__ void __launch_bounds__(256) diffuse_step_kernel(const uint32_t* __res
 }
 
 // ---------------------------------------------------------------------------------------
-// K steps per launch through shared memory (temporal blocking).  CTA (tile_x, tile_y,
-// field) stages padded words [tx0, tx0 + 128) of interior rows [ty0 - K, ty0 - K + 72)
-// (tx0 = tile_x * 120: interior columns tx0 - 4 .. tx0 + 123), runs K steps and writes
-// interior rows [ty0, ty0 + 72 - 2K) x columns [tx0, tx0 + 120).  Warp w marches rows
-// [9w, 9w + 9) of the tile; lane l owns words [4l, 4l + 4).
-template <int K>
-__global__ void __launch_bounds__(kTbWarps * 32) diffuse_tblock_kernel(const uint32_t* __restrict__ src,
-                                                                       uint32_t* __restrict__ dst,
-                                                                       int64_t pitch, int64_t fstride, int H,
-                                                                       int W, const __grid_constant__ Rates rates) {
-    extern __shared__ uint4 smem[];
-    uint4* buf0 = smem;                       // [kTbRows][32]
-    uint4* buf1 = smem + kTbRows * 32;
-    constexpr int TH = kTbRows - 2 * K;       // written rows per tile
+// K steps per launch, the tile held in registers (temporal blocking).  CTA (tile_x, tile_y,
+// field) loads padded words [tx0, tx0 + 128) (tx0 = tile_x * (128 - 2 HALO) + 4 - HALO) of the
+// NW * RPW interior rows starting at ty0 - K; warp w keeps rows [RPW w, RPW w + RPW) of the
+// tile in registers, lane l words [4l, 4l + 4).  Per step a warp publishes the shares of its
+// first and last row in shared memory (double-buffered by step parity: one barrier per
+// step), reads its neighbours' and updates its RPW rows in place; left/right shares come by
+// __shfl (the tile's outermost lanes read their own share instead: those words are halo,
+// invalid after one step and never written).  After K steps the valid region is the tile
+// shrunk by K rows and K words on each side; the CTA writes rows [K, NW*RPW - K) of words
+// [HALO, 128 - HALO).  Tiles that touch the grid edge (or the padding) force the cells
+// outside the grid back to 0 after every step (the padding points of PAPER.md:570, held at
+// 0 by one AND per cell); the other tiles skip the mask.
+template <int K, int NW, int RPW, bool MASK>
+__device__ __forceinline__ void tblock_run(uint4 (&v)[RPW], uint4* pub, int w, int lane, uint32_t a,
+                                           uint4 cm, uint32_t rmask) {
+#pragma unroll 1
+    for (int step = 0; step < K; ++step) {
+        uint4 s[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) s[r] = share4(v[r], a);
+        uint4* top = pub + (step & 1) * (2 * NW * 32);  // [NW][32] first-row shares
+        uint4* bot = top + NW * 32;                     // [NW][32] last-row shares
+        top[w * 32 + lane] = s[0];
+        bot[w * 32 + lane] = s[RPW - 1];
+        __syncthreads();
+        const uint4 zero = make_uint4(0, 0, 0, 0);
+        const uint4 eu = w > 0 ? bot[(w - 1) * 32 + lane] : zero;
+        const uint4 ed = w < NW - 1 ? top[(w + 1) * 32 + lane] : zero;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const uint4 su = r == 0 ? eu : s[r - 1];
+            const uint4 sd = r == RPW - 1 ? ed : s[r + 1];
+            const uint32_t sl = __shfl_up_sync(0xffffffffu, s[r].w, 1);
+            const uint32_t sr = __shfl_down_sync(0xffffffffu, s[r].x, 1);
+            uint4 o = update4(v[r], s[r], su, sd, sl, sr);
+            if (MASK) {
+                const uint32_t rm = (rmask >> r) & 1u ? 0xffffffffu : 0u;
+                o.x &= cm.x & rm;
+                o.y &= cm.y & rm;
+                o.z &= cm.z & rm;
+                o.w &= cm.w & rm;
+            }
+            v[r] = o;
+        }
+    }
+}
+
+template <int K, int NW, int RPW>
+__global__ void __launch_bounds__(NW * 32) diffuse_tblock_kernel(const uint32_t* __restrict__ src,
+                                                                 uint32_t* __restrict__ dst, int64_t pitch,
+                                                                 int64_t fstride, int H, int W,
+                                                                 const __grid_constant__ Rates rates) {
+    constexpr int HALO = K <= 4 ? 4 : 8;        // words on each side (whole lanes)
+    constexpr int OUTC = 128 - 2 * HALO;         // written words per row
+    constexpr int TH = NW * RPW - 2 * K;         // written rows per tile
+    __shared__ uint4 pub[2 * 2 * NW * 32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int field = blockIdx.z;
     const uint32_t a = rates.a[field];
-    const int64_t tx0 = (int64_t)blockIdx.x * kTbOutCols;  // padded column of the tile's word 0
-    const int ty0 = blockIdx.y * TH;                       // first written interior row
-    const int gx = (int)tx0 - (int)kColPad + lane * 4;     // interior column of the lane's .x
-    const int64_t pc = tx0 + lane * 4;                     // padded column of the lane's .x
+    // padded column of the tile's word 0: word HALO is interior column blockIdx.x * OUTC
+    const int64_t tx0 = (int64_t)blockIdx.x * OUTC + kColPad - HALO;
+    const int ty0 = blockIdx.y * TH;                     // first written interior row
+    const int gx = (int)tx0 - (int)kColPad + lane * 4;   // interior column of the lane's .x
+    const int64_t pc = tx0 + lane * 4;                   // padded column of the lane's .x
+    const bool col_in_alloc = pc >= 0 && pc + 4 <= pitch; // pc, pitch: multiples of 4
+    const int gy0 = ty0 - K + w * RPW;                   // interior row of the warp's row 0
     const uint32_t* s = src + (int64_t)field * fstride + pc;
-    const bool col_in_alloc = pc + 4 <= pitch;
-    // per-cell interior column mask, fixed for the whole launch
-    const bool c0 = gx >= 0 && gx < W, c1 = gx + 1 >= 0 && gx + 1 < W;
-    const bool c2 = gx + 2 >= 0 && gx + 2 < W, c3 = gx + 3 >= 0 && gx + 3 < W;
-    const int row0 = w * kTbRowsPerWarp;
-
-    // stage: tile row r <-> interior row ty0 - K + r <-> padded row ty0 - K + r + 1
+    uint4 v[RPW];
 #pragma unroll
-    for (int r = 0; r < kTbRowsPerWarp; ++r) {
-        const int pr = ty0 - K + row0 + r + 1;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (pr >= 0 && pr < H + 2 && col_in_alloc) v = ldg4(s + (int64_t)pr * pitch);
-        buf0[(row0 + r) * 32 + lane] = v;
+    for (int r = 0; r < RPW; ++r) {
+        const int pr = gy0 + r + 1;
+        v[r] = (pr >= 0 && pr < H + 2 && col_in_alloc) ? ldg4(s + (int64_t)pr * pitch) : make_uint4(0, 0, 0, 0);
     }
-    __syncthreads();
-
-#pragma unroll 1
-    for (int step = 1; step <= K; ++step) {
-        const uint4* cur = (step & 1) ? buf0 : buf1;
-        uint4* nxt = (step & 1) ? buf1 : buf0;
-        const bool last = step == K;
-        // rows outside [step, kTbRows - step) are no longer valid after this step
-        const int lo = max(row0, last ? K : step);
-        const int hi = min(row0 + kTbRowsPerWarp, last ? K + TH : kTbRows - step);
-        if (lo < hi) {  // warp-uniform
-            uint4 sc = share4(cur[lo * 32 + lane], a);
-            uint4 vc = cur[lo * 32 + lane];
-            uint4 su = share4(cur[(lo - 1) * 32 + lane], a);  // lo >= 1
-            for (int row = lo; row < hi; ++row) {
-                const uint4 vd = cur[(row + 1) * 32 + lane];   // row + 1 <= kTbRows - 1
-                const uint4 sd = share4(vd, a);
-                uint32_t sl = __shfl_up_sync(0xffffffffu, sc.w, 1);
-                uint32_t sr = __shfl_down_sync(0xffffffffu, sc.x, 1);
-                if (lane == 0) sl = 0;   // beyond the tile: garbage halo, never read back
-                if (lane == 31) sr = 0;
-                uint4 o = update4(vc, sc, su, sd, sl, sr);
-                const int gy = ty0 - K + row;
-                const bool rin = gy >= 0 && gy < H;
-                o.x = (rin && c0) ? o.x : 0u;  // padding points stay 0
-                o.y = (rin && c1) ? o.y : 0u;
-                o.z = (rin && c2) ? o.z : 0u;
-                o.w = (rin && c3) ? o.w : 0u;
-                if (!last) {
-                    nxt[row * 32 + lane] = o;
-                } else if (rin && lane >= 1 && lane <= 30 && gx < W) {
-                    store4(dst + (int64_t)field * fstride + (int64_t)(gy + 1) * pitch + pc, o, W - gx);
-                }
-                su = sc;
-                sc = sd;
-                vc = vd;
-            }
-        }
-        if (!last) __syncthreads();
+    // does the tile (with its halo) reach outside the grid?  CTA-uniform.
+    const bool edge = ty0 - K < 0 || ty0 - K + NW * RPW > H || (int)tx0 - (int)kColPad < 0 ||
+                      (int)tx0 - (int)kColPad + 128 > W;
+    if (edge) {
+        const uint4 cm = make_uint4(gx >= 0 && gx < W ? ~0u : 0u, gx + 1 >= 0 && gx + 1 < W ? ~0u : 0u,
+                                    gx + 2 >= 0 && gx + 2 < W ? ~0u : 0u, gx + 3 >= 0 && gx + 3 < W ? ~0u : 0u);
+        uint32_t rmask = 0;
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) rmask |= (gy0 + r >= 0 && gy0 + r < H) ? (1u << r) : 0u;
+        tblock_run<K, NW, RPW, true>(v, pub, w, lane, a, cm, rmask);
+    } else {
+        tblock_run<K, NW, RPW, false>(v, pub, w, lane, a, make_uint4(0, 0, 0, 0), 0u);
+    }
+    if (lane < HALO / 4 || lane >= 32 - HALO / 4 || gx >= W) return;
+    uint32_t* d = dst + (int64_t)field * fstride + pc;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+        const int row = w * RPW + r, gy = gy0 + r;
+        if (row >= K && row < K + TH && gy < H) store4(d + (int64_t)(gy + 1) * pitch, v[r], W - gx);
     }
 }
 
@@ -296,16 +319,12 @@ sw_status_t launch_step(const uint32_t* src, uint32_t* dst, int64_t pitch, int64
 template <int K>
 sw_status_t launch_tblock_k(const uint32_t* src, uint32_t* dst, int64_t pitch, int64_t fstride, int H, int W,
                             int n_fields, const Rates& rates, cudaStream_t st) {
-    constexpr int TH = kTbRows - 2 * K;
-    const size_t smem = 2 * (size_t)kTbRows * kTbCols * sizeof(uint32_t);
-    static bool attr = false;  // per process; the attribute is per device function
-    if (!attr) {
-        cudaFuncSetAttribute(diffuse_tblock_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    dim3 grid((unsigned)((W + kTbOutCols - 1) / kTbOutCols), (unsigned)((H + TH - 1) / TH), (unsigned)n_fields);
+    constexpr int HALO = K <= 4 ? 4 : 8, TH = kTbWarps * kTbRowsPerWarp - 2 * K;
+    dim3 grid((unsigned)((W + 128 - 2 * HALO - 1) / (128 - 2 * HALO)), (unsigned)((H + TH - 1) / TH),
+              (unsigned)n_fields);
     if (grid.y > 65535u) return fail(SW_ERR_INVALID_ARGUMENT, "grid too tall for the temporal-blocking schedule");
-    diffuse_tblock_kernel<K><<<grid, kTbWarps * 32, smem, st>>>(src, dst, pitch, fstride, H, W, rates);
+    diffuse_tblock_kernel<K, kTbWarps, kTbRowsPerWarp><<<grid, kTbWarps * 32, 0, st>>>(src, dst, pitch, fstride, H,
+                                                                                        W, rates);
     ++g_launches;
     return check_launch("diffuse_tblock_kernel");
 }
@@ -317,6 +336,10 @@ sw_status_t launch_k(int k, const uint32_t* src, uint32_t* dst, int64_t pitch, i
         case 2: return launch_tblock_k<2>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
         case 3: return launch_tblock_k<3>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
         case 4: return launch_tblock_k<4>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
+        case 5: return launch_tblock_k<5>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
+        case 6: return launch_tblock_k<6>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
+        case 7: return launch_tblock_k<7>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
+        case 8: return launch_tblock_k<8>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
         default: return fail(SW_ERR_INTERNAL, "bad steps per launch");
     }
 }
@@ -396,8 +419,8 @@ sw_status_t simcov_diffuse(uint32_t* grid, uint32_t* scratch, int64_t H, int64_t
     // the launch plan: steps per launch, an even number of launches so the result lands in grid
     int kmax = g_schedule;
     if (kmax == 0) kmax = kTbMaxK;
-    if (kmax > kTbMaxK) kmax = kTbMaxK;
-    if ((H + kTbRows - 2 * kTbMaxK - 1) / (kTbRows - 2 * kTbMaxK) > 65535) kmax = 1;  // grid.y limit
+    if (kmax > SIMCOV_MAX_TBLOCK) kmax = SIMCOV_MAX_TBLOCK;
+    if ((H + kTbWarps * kTbRowsPerWarp - 2 * 8 - 1) / (kTbWarps * kTbRowsPerWarp - 2 * 8) > 65535) kmax = 1;  // grid.y limit
     if (kmax == 1 || steps == 1) {
         // one step per launch (marching kernel); odd counts end with a copy back
         uint32_t *a = grid, *b = scratch;

@@ -15,7 +15,7 @@ from . import sw
 
 SIMCOV_MAX_FIELDS = 8
 SIMCOV_MAX_RATE = 1 << 30
-SIMCOV_MAX_TBLOCK = 4
+SIMCOV_MAX_TBLOCK = 8
 
 EXPORTED = ("simcov_grid_pitch", "simcov_grid_words", "simcov_pad", "simcov_unpad", "simcov_diffuse",
             "simcov_set_schedule", "simcov_last_launch_count", "simcov_last_error_message")

@@ -38,7 +38,7 @@ def main():
     g = simcov.Grid(H, W, 2)
     g.upload(fields)
     cells = 2 * H * W
-    for sch in (1, 2, 3, 4):
+    for sch in [int(x) for x in os.environ.get("SCHEDULES", "1,2,3,4,5,6,7,8").split(",")]:
         simcov.simcov_set_schedule(sch)
         ms = time_one(g, rates, steps)
         n = simcov.simcov_last_launch_count() - 2
