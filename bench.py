@@ -226,6 +226,66 @@ def time_device_steps(a, q, qo, r, ro, scoring, out, steps, warmup, flush_buf, t
     return times, stage
 
 
+def simcov_extra(torch, no_cpu: bool) -> dict:
+    """the diffusion stencil (include/simcov.h) on two SIMCoV-shaped fields.
+    Unit: cell-steps/s (one field cell advanced by one step).  The one-step kernel is
+    HBM-bound (8 algorithmic bytes per cell-step: one read, one write); the temporal-blocking
+    schedule (default) moves 8 B per cell per launch of k steps."""
+    from paper_2208_12350_b200 import simcov, synth
+    hbm = None
+    try:
+        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except (OSError, ValueError, KeyError):
+        hbm, hbm_src = 6650.0, "B200_PROFILING.md fallback"
+    rates = [simcov.rate_fixed(0.2), simcov.rate_fixed(0.1)]
+    res = {}
+    for name, (H, W) in (("grid_16384", (16384, 16384)), ("heldout_2500", synth.SIMCOV_HELDOUT)):
+        steps = 24
+        g = simcov.Grid(H, W, 2)
+        g.upload(synth.simcov_fields(5, H, W, 2, peak=1 << 26, background=0.05))
+        cells = 2 * H * W
+        row = {"workload": f"2 fields (virions, inflammatory signal) {H}x{W}, {steps} steps per simcov_diffuse call",
+               "inputs_vs_l2": "2 x 2 x 1 GiB > L2" if H > 4096 else "2 x 2 x 25 MB: L2-resident between launches"}
+        for sch in (0, 1):
+            simcov.simcov_set_schedule(sch)
+            g.diffuse(rates, steps)
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(5):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.diffuse(rates, steps)
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = float(np.median(ts))
+            launches = simcov.simcov_last_launch_count()
+            key = "default" if sch == 0 else "one_step_per_launch"
+            row[key] = {"ms": round(ms, 4), "gcell_steps_per_s": round(cells * steps / ms / 1e6, 1),
+                        "launches": launches,
+                        "alg_hbm_GBps": round(8 * cells * (launches - 2) / ms / 1e6, 1)}
+        simcov.simcov_set_schedule(0)
+        one = row["one_step_per_launch"]
+        row["roofline_one_step"] = {"bound": "hbm", "achieved": one["alg_hbm_GBps"], "peak": hbm, "unit": "GB/s",
+                                    "frac": round(one["alg_hbm_GBps"] / hbm, 4), "peak_source": hbm_src,
+                                    "bytes_per_cell_step": 8}
+        row["speedup_default_vs_one_step"] = round(one["ms"] / row["default"]["ms"], 3)
+        res[name] = row
+        del g
+    if not no_cpu:
+        from oracle import diffusion as D
+        H, W = synth.SIMCOV_HELDOUT
+        f = synth.simcov_fields(5, H, W, 2, peak=1 << 26, background=0.05)
+        t0 = time.perf_counter()
+        D.diffuse(f, rates, 2)
+        dt = time.perf_counter() - t0
+        res["cpu_oracle"] = {"gcell_steps_per_s": round(2 * H * W * 2 / dt / 1e9, 4), "cores": 1, "kind": "oracle",
+                             "sample": f"2 fields {H}x{W}, 2 steps, numpy, {dt:.2f} s"}
+    return res
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
@@ -367,6 +427,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                               "interval_cells": icells, "interval_gcups": round(icells / med / 1e6, 1),
                               "pairs_per_s": round(batch.n_pairs / med * 1e3, 1),
                               "ops_total": int(n_ops[:batch.n_pairs].clamp(min=0).sum().item())}
+
+    if rank == 0 and not args.no_extra:
+        extra["simcov"] = simcov_extra(torch, args.no_cpu_baseline)
 
     cpu = None
     parity = None

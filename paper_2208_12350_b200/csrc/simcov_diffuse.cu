@@ -16,13 +16,14 @@
 //   marches down R rows keeping the rows above and below in registers (each
 //   word is loaded once), left/right neighbour shares by __shfl (only the two
 //   strip-edge lanes load a scalar from the padding or the next strip);
-// * temporal blocking (k <= 4 steps per launch): a CTA stages a 128-word x
-//   (64 + 2k)-row tile in shared memory, runs k steps there (the valid region
-//   shrinks by one cell per step) and writes only its 120 x 64 core, so HBM
-//   traffic is 8 B per cell per k steps plus the halo re-reads.  Inside the tile
-//   the cells outside the grid are forced back to 0 after every step -- the same
-//   padding points, now held at 0 in shared memory by one select per cell
-//   (a per-thread column mask computed once, a row compare per row).
+// * temporal blocking (k <= 8 steps per launch, the default schedule): a CTA of 8 warps
+//   loads a 128-word x 160-row tile straight into registers (20 rows per warp), runs k
+//   steps there -- only the first/last-row shares of each warp cross through shared
+//   memory, one barrier per step -- and writes its core (the tile shrunk by k rows and a
+//   4- or 8-word halo), so HBM traffic is 8 B per cell per k steps plus the halo re-reads.
+//   Tiles reaching outside the grid force the cells outside it back to 0 after every step
+//   -- the same padding points, held at 0 by one AND per cell (a per-thread column mask
+//   computed once, a per-row bit); interior tiles skip the mask.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -45,10 +46,13 @@ constexpr int kStripCols = 128;  // one warp: 32 lanes x 4 cells
 #define SIMCOV_TB_WARPS 8
 #endif
 #ifndef SIMCOV_TB_RPW
-#define SIMCOV_TB_RPW 16
+#define SIMCOV_TB_RPW 20
+#endif
+#ifndef SIMCOV_TB_MINB
+#define SIMCOV_TB_MINB 2
 #endif
 #ifndef SIMCOV_TB_KMAX
-#define SIMCOV_TB_KMAX 6
+#define SIMCOV_TB_KMAX 8
 #endif
 constexpr int kTbMaxK = SIMCOV_TB_KMAX;  // default steps per launch (halo 4 words for k <= 4, else 8)
 constexpr int kTbWarps = SIMCOV_TB_WARPS;
@@ -156,24 +160,25 @@ __device__ __forceinline__ void tblock_run(uint4 (&v)[RPW], uint4* pub, int w, i
                                            uint4 cm, uint32_t rmask) {
 #pragma unroll 1
     for (int step = 0; step < K; ++step) {
-        uint4 s[RPW];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) s[r] = share4(v[r], a);
+        // shares are formed on the fly (three rows live), so the tile itself is most of
+        // the register budget; only the first and last row's shares are formed up front
+        const uint4 sfirst = share4(v[0], a), slast = share4(v[RPW - 1], a);
         uint4* top = pub + (step & 1) * (2 * NW * 32);  // [NW][32] first-row shares
         uint4* bot = top + NW * 32;                     // [NW][32] last-row shares
-        top[w * 32 + lane] = s[0];
-        bot[w * 32 + lane] = s[RPW - 1];
+        top[w * 32 + lane] = sfirst;
+        bot[w * 32 + lane] = slast;
         __syncthreads();
         const uint4 zero = make_uint4(0, 0, 0, 0);
-        const uint4 eu = w > 0 ? bot[(w - 1) * 32 + lane] : zero;
+        uint4 su = w > 0 ? bot[(w - 1) * 32 + lane] : zero;
         const uint4 ed = w < NW - 1 ? top[(w + 1) * 32 + lane] : zero;
+        uint4 sc = sfirst;
 #pragma unroll
         for (int r = 0; r < RPW; ++r) {
-            const uint4 su = r == 0 ? eu : s[r - 1];
-            const uint4 sd = r == RPW - 1 ? ed : s[r + 1];
-            const uint32_t sl = __shfl_up_sync(0xffffffffu, s[r].w, 1);
-            const uint32_t sr = __shfl_down_sync(0xffffffffu, s[r].x, 1);
-            uint4 o = update4(v[r], s[r], su, sd, sl, sr);
+            // v[r + 1] still holds the previous step's value here
+            const uint4 sd = r == RPW - 1 ? ed : (r == RPW - 2 ? slast : share4(v[r + 1], a));
+            const uint32_t sl = __shfl_up_sync(0xffffffffu, sc.w, 1);
+            const uint32_t sr = __shfl_down_sync(0xffffffffu, sc.x, 1);
+            uint4 o = update4(v[r], sc, su, sd, sl, sr);
             if (MASK) {
                 const uint32_t rm = (rmask >> r) & 1u ? 0xffffffffu : 0u;
                 o.x &= cm.x & rm;
@@ -182,12 +187,14 @@ __device__ __forceinline__ void tblock_run(uint4 (&v)[RPW], uint4* pub, int w, i
                 o.w &= cm.w & rm;
             }
             v[r] = o;
+            su = sc;
+            sc = sd;
         }
     }
 }
 
 template <int K, int NW, int RPW>
-__global__ void __launch_bounds__(NW * 32) diffuse_tblock_kernel(const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(NW * 32, SIMCOV_TB_MINB) diffuse_tblock_kernel(const uint32_t* __restrict__ src,
                                                                  uint32_t* __restrict__ dst, int64_t pitch,
                                                                  int64_t fstride, int H, int W,
                                                                  const __grid_constant__ Rates rates) {
