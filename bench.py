@@ -517,11 +517,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank)
         return
+    # SW_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0 over gloo, so the N > 1 code path
+    # (shard plan, barriers, max-over-ranks) can be exercised on a one-GPU box; not a measurement
+    shared = os.environ.get("SW_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -15,7 +15,7 @@ from paper_2208_12350_b200 import simcov, synth
 
 pytestmark = pytest.mark.gpu
 
-SCHEDULES = (0, 1, 2, 3, 4)
+SCHEDULES = (0, 1, 2, 3, 4, 8)
 
 
 @pytest.fixture(autouse=True)
@@ -127,10 +127,18 @@ def test_launch_plan_counts():
     fields = synth.simcov_fields(2, 64, 64, 1)
     g = simcov.Grid(64, 64, 1)
     g.upload(fields)
+    simcov.simcov_set_schedule(4)
     g.diffuse([simcov.rate_fixed(0.1)], 16)
     assert simcov.simcov_last_launch_count() == 2 + 4  # ring zeroing x2, four 4-step launches
     g.diffuse([simcov.rate_fixed(0.1)], 5)
     assert simcov.simcov_last_launch_count() == 2 + 2  # (4, 1)
+    simcov.simcov_set_schedule(0)
+    g.diffuse([simcov.rate_fixed(0.1)], 16)
+    assert simcov.simcov_last_launch_count() == 2 + 2  # default: (8, 8)
+    g.diffuse([simcov.rate_fixed(0.1)], 5)
+    assert simcov.simcov_last_launch_count() == 2 + 2  # 5 -> (2, 3): an even count ends in grid
+    g.diffuse([simcov.rate_fixed(0.1)], 1)
+    assert simcov.simcov_last_launch_count() == 2 + 1  # one step, then a copy back (not a kernel)
 
 
 def test_argument_errors():
