@@ -172,37 +172,52 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         uint8_t* out = P.ops + (P.q_off[p] - P.q0) + (P.r_off[p] - P.r0);
         int len = 0;
         if (lane == 0) {
-            auto bits = [&](int i, int j) -> uint32_t {  // 1-based interior cell
-                const int s = (i - 1) / TB_ROWS, L = ((i - 1) % TB_ROWS) / TB_K, r = (i - 1) % TB_K;
-                const int t = j - 1 + L;
-                return (dir[(int64_t)(s * 32 + L) * steps_pad + t] >> (5 * r)) & 31u;
-            };
-            // H's preferred move at (i, j): 0 diagonal, 1 F, 2 E (border cells: no diagonal; H == F on column 0)
-            auto pref = [&](int i, int j) -> int {
-                if (i >= 1 && j >= 1) return (int)(bits(i, j) & 3u);
-                return j == 0 && i >= 1 ? 1 : 2;
-            };
+            // position of cell (i, j) (1-based) in the direction words: row i - 1 lives in stripe
+            // s, lane L, bit group r; its word for column j is dir[rowoff + j] with
+            // rowoff = (32 s + L) * steps_pad + L - 1.  The walk keeps (r, rowoff) and the current
+            // word incrementally: an up move inside a lane's 5 rows reuses the word, every other
+            // move loads exactly the word the next decision needs.
             int i = a, j = b, state = 0;
+            int r = (a - 1) % TB_K, Lc = ((a - 1) % TB_ROWS) / TB_K;
+            int64_t rowoff = (int64_t)(((a - 1) / TB_ROWS) * 32 + Lc) * steps_pad + Lc - 1;
+            uint32_t w = dir[rowoff + j];
             bool bad = false;
+            // one row up: returns true when the row's word lives in another lane's line
+            auto up = [&]() -> bool {
+                --i;
+                if (r > 0) { --r; return false; }
+                r = TB_K - 1;
+                if (Lc > 0) { --Lc; rowoff -= steps_pad + 1; }
+                else { Lc = 31; rowoff += 31 - steps_pad; }
+                return true;
+            };
             while (i > 0 || j > 0) {
                 if (i == 0 || j == 0) { bad = true; break; }  // optimal paths start with an aligned pair
-                const uint32_t c = bits(i, j);
+                const uint32_t c = (w >> (5 * r)) & 31u;
                 if (state == 0) {
                     const int pr = (int)(c & 3u);
-                    if (pr == 0) { out[len++] = 'M'; --i; --j; }
-                    else state = pr;  // 1: F, 2: E
+                    if (pr == 0) {
+                        out[len++] = 'M';
+                        up();
+                        --j;
+                        if (i > 0 && j > 0) w = dir[rowoff + j];
+                    } else {
+                        state = pr;  // 1: F, 2: E
+                    }
                 } else if (state == 1) {
                     out[len++] = 'I';
                     const bool open = c & 4u, ext = c & 8u;
-                    const int up = pref(i - 1, j);
-                    state = (open && up == 0) ? 0 : ((ext || (open && up == 1)) ? 1 : 0);
-                    --i;
+                    if (up() && i > 0) w = dir[rowoff + j];
+                    // H's preferred move of the cell above (row 0 is the border: E)
+                    const int upr = i >= 1 ? (int)((w >> (5 * r)) & 3u) : 2;
+                    state = (open && upr == 0) ? 0 : ((ext || (open && upr == 1)) ? 1 : 0);
                 } else {
                     out[len++] = 'D';
                     const bool open = c & 16u;
-                    const int left = pref(i, j - 1);
-                    state = (open && left != 2) ? 0 : 2;
                     --j;
+                    int left = 1;  // column 0 (i >= 1): H == F
+                    if (j >= 1) { w = dir[rowoff + j]; left = (int)((w >> (5 * r)) & 3u); }
+                    state = (open && left != 2) ? 0 : 2;
                 }
             }
             if (bad || len > a + b) { len = -1; atomicAdd(P.err, 1); }
