@@ -75,6 +75,7 @@ struct sw_context {
     int max_occ_cached_nc = -1;
     cudaStream_t last_stream = nullptr;
     bool have_last = false;
+    bool no_spec_ext = false;  // force the synchronous extent read (after a speculative overflow)
     std::string err;
 
     // per-pair
@@ -347,12 +348,16 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     h->have_last = true;
 
     // 1. payload extents
-    int64_t ext[4];
+    int64_t ext[4] = {0, 0, 0, 0};
+    // speculative extents (device-buffer calls once the code buffers exist): pack reads the
+    // extents itself and checks they fit the buffers' capacity; the host learns the outcome from
+    // the statistics read-back it does anyway (one host round trip per call instead of two)
+    const bool spec = !hp && !host_ext && !h->no_spec_ext && h->qcode.cap > 0 && h->rcode.cap > 0 && h->rrev.cap > 0;
     if (hp) {
         std::memcpy(ext, hp->ext, sizeof(ext));
     } else if (host_ext) {
         std::memcpy(ext, host_ext, sizeof(ext));
-    } else {
+    } else if (!spec) {
         SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 0, q_off, 8, cudaMemcpyDeviceToHost, s));
         SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 1, q_off + n_pairs, 8, cudaMemcpyDeviceToHost, s));
         SW_CUDA(h, cudaMemcpyAsync(h->h_ext + 2, r_off, 8, cudaMemcpyDeviceToHost, s));
@@ -368,8 +373,8 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     }
     const size_t tq = (size_t)(qN - q0), tr = (size_t)(rN - r0);
     // code buffers keep the payloads' 16-byte phase so pack moves aligned vectors
-    const int64_t qshift = (int64_t)(((uintptr_t)(queries + q0)) & 15);
-    const int64_t rshift = (int64_t)(((uintptr_t)(refs + r0)) & 15);
+    const int64_t qshift = spec ? 0 : (int64_t)(((uintptr_t)(queries + q0)) & 15);
+    const int64_t rshift = spec ? 0 : (int64_t)(((uintptr_t)(refs + r0)) & 15);
 
     // 2. workspace
     st = prepare_workspace(h, N, tq, tr, sc.alphabet, s);
@@ -392,6 +397,8 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
         P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA) ? 1 : 0;  // TAG route: DNA batches
         P.rows_s16 = rows16; P.rows_s32 = rows32;
+        P.ext_dev = spec ? 1 : 0; P.n_all = n_pairs;
+        P.qcap = (int64_t)h->qcode.cap; P.rcap = (int64_t)std::min(h->rcode.cap, h->rrev.cap);
         P.qcode = h->qcode.p; P.rcode = h->rcode.p;
         P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
         P.hist = hist; P.keys_fwd = h->keys_fwd.p; P.iota = h->iota.p; P.stats = stats;
@@ -403,6 +410,14 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         ++h->own_launches;
     }
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
+    // forward binning enqueued before the read-back below, assuming the common small-region
+    // batch: the GPU bins while the host waits; a batch outside it is re-sorted (radix) after
+    const bool spec_bin = !hp;
+    if (spec_bin) {
+        st = bin_order(h, h->order.p + lo, lo, hi, true, slot, s);
+        if (st != SW_OK) return st;
+        SW_CUDA(h, cudaMemsetAsync(counters, 0, 8 * sizeof(int32_t), s));  // work queues (step 6)
+    }
     // 4. statistics -> grids and scratch (read back, unless the host already knows bounds)
     BatchStats hs;
     if (hp) {
@@ -414,6 +429,12 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         SW_CUDA(h, cudaMemcpyAsync(h->h_stats, stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
         SW_CUDA(h, cudaStreamSynchronize(s));
         hs = *h->h_stats;
+    }
+    if (hs.overflow) {  // speculative extents did not fit: grow with the synchronous read, re-run
+        h->no_spec_ext = true;
+        st = align_impl(h, queries, q_off, refs, r_off, n_pairs, scoring, out, s, nullptr, nullptr);
+        h->no_spec_ext = false;
+        return st;
     }
     if (hs.malformed) {
         SW_CUDA(h, cudaMemsetAsync(hist, 0, NBINS * sizeof(uint32_t), s));  // pack binned some pairs
@@ -471,12 +492,14 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     const int min_rows = std::min(rows16, rows32);
     const bool small_fwd = hs.max_m < BIN_COLS && (hs.max_n + min_rows - 1) / min_rows <= BIN_MAX_STRIPES;
     const bool small_rev = small_fwd && (int64_t)sc.max_sigma * std::min(hs.max_n, hs.max_m) < BIN_COLS;
-    st = bin_order(h, h->order.p + lo, lo, hi, small_fwd, slot, s);
-    if (st != SW_OK) return st;
+    if (!spec_bin || !small_fwd) {
+        st = bin_order(h, h->order.p + lo, lo, hi, small_fwd, slot, s);
+        if (st != SW_OK) return st;
+    }
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[3], s));
 
     // 6. forward wavefront
-    SW_CUDA(h, cudaMemsetAsync(counters, 0, 8 * sizeof(int32_t), s));
+    if (!spec_bin) SW_CUDA(h, cudaMemsetAsync(counters, 0, 8 * sizeof(int32_t), s));
     WaveParams W;
     W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch[slot].p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
     W.tag_mul = 64;

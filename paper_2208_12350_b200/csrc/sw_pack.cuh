@@ -20,7 +20,7 @@ struct BatchStats {
     int32_t max_n;          // longest valid query
     int32_t max_m;          // longest valid reference
     int32_t malformed;      // offsets decrease somewhere -> whole batch invalid
-    int32_t pad_;
+    int32_t overflow;       // speculative extents: the payload did not fit the code buffers (nothing packed)
     int32_t fwd_count[4];   // valid, non-trivial pairs per route (forward pass)
     int32_t rev_count[4];   // pairs with S > 0 per route (reverse pass)
 };
@@ -32,8 +32,11 @@ struct PackParams {
     const uint8_t* refs;
     const int64_t* r_off;
     int64_t lo, hi;              // pairs to pack (positions in the code buffers are batch-global)
-    int64_t q0, qN, r0, rN;      // payload extents of the whole batch (host-read)
+    int64_t q0, qN, r0, rN;      // payload extents of the whole batch (host-read, unless ext_dev)
     int64_t qshift, rshift;      // (payload + extent start) mod 16: code buffers keep the payload's alignment
+    int ext_dev;                 // read the extents from q_off / r_off here (no host round trip) and check
+    int64_t n_all;               //   they fit qcap / rcap (else stats->overflow, nothing written)
+    int64_t qcap, rcap;
     int alphabet;
     int s16_ok;                  // scoring fits the s16x2 path (int8 profile, int16 range)
     int tag_ok;                  // the ROUTE_TAG kernel geometry supports row tags
@@ -181,6 +184,22 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
     const int wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t q0 = P.q0, qN = P.qN, r0 = P.r0, rN = P.rN, qshift = P.qshift, rshift = P.rshift;
+    if (P.ext_dev) {
+        // extents of the whole batch, read by every thread (one L2 line each): the host skips the
+        // synchronous read-back and sized the code buffers from their current capacity
+        q0 = P.q_off[0]; qN = P.q_off[P.n_all]; r0 = P.r_off[0]; rN = P.r_off[P.n_all];
+        qshift = (int64_t)(((uintptr_t)(P.queries + q0)) & 15);
+        rshift = (int64_t)(((uintptr_t)(P.refs + r0)) & 15);
+        if (qN < q0 || rN < r0) {  // the host reports it after the statistics read-back
+            if (blockIdx.x == 0 && threadIdx.x == 0) P.stats->malformed = 1;
+            return;
+        }
+        if ((qN - q0) + 32 > P.qcap || (rN - r0) + P.n_all * (PADL + PADR) + GUARD + 16 > P.rcap) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) P.stats->overflow = 1;
+            return;  // uniform over the grid: nothing is written, the host grows and re-runs
+        }
+    }
     const uint8_t pad_code = (uint8_t)((P.alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN) - 1);
     const uint32_t padw = (uint32_t)pad_code * 0x01010101u;
     const bool dna = P.alphabet == SW_ALPHABET_DNA;
@@ -197,10 +216,10 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
         int64_t qa = 0, qb = 0, ra = 0, rb = 0;
         if (act) { qa = P.q_off[p]; qb = P.q_off[p + 1]; ra = P.r_off[p]; rb = P.r_off[p + 1]; }
         const int64_t n = qb - qa, m = rb - ra;
-        const bool malf = act && (n < 0 || m < 0 || qa < P.q0 || qb > P.qN || ra < P.r0 || rb > P.rN);
+        const bool malf = act && (n < 0 || m < 0 || qa < q0 || qb > qN || ra < r0 || rb > rN);
         if (malf) l_malf = 1;
-        const int64_t qp = (qa - P.q0) + P.qshift;
-        const int64_t rp = (ra - P.r0) + (p + 1) * PADL + p * PADR + P.rshift;
+        const int64_t qp = (qa - q0) + qshift;
+        const int64_t rp = (ra - r0) + (p + 1) * PADL + p * PADR + rshift;
         if (lane == 0) s_badbits[wib] = 0u;
         if (!__any_sync(FULL, malf)) {
             if (act) { slot[lane] = rp - PADL; rdelta[lane] = ra - rp; sm[lane] = (int32_t)m; sqa[lane] = qa; }
@@ -226,7 +245,7 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
                     if (a < b) {
                         rs[u] = (int)(a - y0); re[u] = (int)(b - y0);
                         const int64_t s0 = y0 + rdelta[k];  // payload index of the vector's byte 0 (16-aligned address)
-                        if (s0 >= P.r0 && s0 + 16 <= P.rN) {  // whole block inside the caller's payload
+                        if (s0 >= r0 && s0 + 16 <= rN) {  // whole block inside the caller's payload
                             src[u] = __ldg(reinterpret_cast<const uint4*>(P.refs + s0));
                         } else {
                             uint32_t w[4] = {0, 0, 0, 0};
@@ -262,9 +281,9 @@ __global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
                 }
             }
             // ---- queries: output vectors of [qlo, qhi) in qcode (no pads; shift qshift - q0) ----
-            const int64_t qlo = __shfl_sync(FULL, qa, 0) - P.q0 + P.qshift;
-            const int64_t qhi = __shfl_sync(FULL, qb, cnt - 1) - P.q0 + P.qshift;
-            const int64_t qd = P.q0 - P.qshift;  // payload index of code position y is y + qd
+            const int64_t qlo = __shfl_sync(FULL, qa, 0) - q0 + qshift;
+            const int64_t qhi = __shfl_sync(FULL, qb, cnt - 1) - q0 + qshift;
+            const int64_t qd = q0 - qshift;  // payload index of code position y is y + qd
             if (qhi > qlo) {
                 const int64_t qv_hi = (qhi - 1) >> 4;
                 for (int64_t vb = qlo >> 4; vb <= qv_hi; vb += 32 * PACK_FB) {

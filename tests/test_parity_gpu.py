@@ -548,3 +548,29 @@ def test_query_db_mode(aligner, alpha):
         b = synth.from_pairs([(query, r) for r in refs], src.scoring)
         got = aligner.align_query_db(query, refs, src.scoring)
         assert_parity(got, oracle_batch(b), b)
+
+
+def test_speculative_extents_grow_and_rerun():
+    """Device-buffer calls read the payload extents inside pack once the code buffers exist
+    (sw_api.cu: speculative extents); a batch larger than the buffers must be detected there,
+    grown and re-run with the same results, and a later smaller batch must reuse the buffers."""
+    a = sw.Aligner(0)
+    try:
+        small = synth.generate("c1", 0, 50)
+        big = synth.generate("c2", 0, 3000)
+        for b in (small, big, small, synth.generate("c3", 0, 400), big):
+            assert_parity(a.align(b), oracle_batch(b), b)
+        # offsets that decrease (qN < q0 of the whole batch) on the speculative path
+        import torch
+        q, qo, r, ro = a.to_device(small)
+        qo_bad = qo.clone()
+        qo_bad[-1] = 0
+        qo_bad[0] = int(qo[-1].item())
+        out = a.alloc_out(small.n_pairs)
+        with pytest.raises(sw.SWError):
+            a.align_tensors(q, qo_bad, r, ro, small.scoring, out=out)
+        torch.cuda.synchronize()
+        assert (out[0, :small.n_pairs] == -1).all()
+        assert_parity(a.align(small), oracle_batch(small), small)
+    finally:
+        a.close()
