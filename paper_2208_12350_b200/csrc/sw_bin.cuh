@@ -90,11 +90,21 @@ __global__ void __launch_bounds__(BIN_SCAN_THREADS) bin_scan_kernel(uint32_t* hi
 }
 
 // order[base[bin(key[p])]++] = p for every pair with work (small-region batches only).
+// Warp-aggregated: lanes holding the same bin (reverse keys cluster on a few scores) take
+// their slots with one atomic per distinct bin of the warp.
 __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint32_t* key, uint32_t* base, int32_t* order, int64_t lo,
                                                          int64_t hi) {
-    for (int64_t p = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < hi; p += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t b = key_bin(key[p]);
-        if (b) order[atomicAdd(base + b, 1u)] = (int32_t)p;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p0 = lo + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); p0 < hi; p0 += stride) {
+        const int64_t p = p0 + lane;
+        const uint32_t b = p < hi ? key_bin(key[p]) : 0u;
+        const uint32_t peers = __match_any_sync(FULL, b);
+        const int leader = __ffs(peers) - 1;
+        uint32_t off = 0;
+        if (b && lane == leader) off = atomicAdd(base + b, (uint32_t)__popc(peers));
+        off = __shfl_sync(FULL, off, leader);
+        if (b) order[off + __popc(peers & ((1u << lane) - 1u))] = (int32_t)p;
     }
 }
 

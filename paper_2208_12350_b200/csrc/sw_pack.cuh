@@ -150,9 +150,18 @@ __device__ __forceinline__ void store16_within(uint8_t* dst, int64_t y0, uint4 v
     }
 }
 
+#ifndef SW_PACK_PPW
+#define SW_PACK_PPW 8
+#endif
+#ifndef SW_PACK_FB
+#define SW_PACK_FB 4
+#endif
+#ifndef SW_PACK_MINB
+#define SW_PACK_MINB 3
+#endif
 constexpr int PACK_WARPS = 8;  // warps per pack block (256 threads)
-constexpr int PACK_PPW = 8;    // pairs per warp
-constexpr int PACK_FB = 4;     // 16-byte vectors per lane in flight
+constexpr int PACK_PPW = SW_PACK_PPW;    // pairs per warp
+constexpr int PACK_FB = SW_PACK_FB;      // 16-byte vectors per lane in flight
 
 // One warp packs PACK_PPW consecutive pairs: lanes read the pairs' offsets,
 // then the warp converts the pairs' reference and query payloads as flat
@@ -163,7 +172,7 @@ constexpr int PACK_FB = 4;     // 16-byte vectors per lane in flight
 // so a vector holds bytes of at most one reference plus pads (one load and a
 // byte mask).  Vectors shared with the neighbouring warp's span are written
 // byte-wise (only this warp's bytes).
-__global__ void __launch_bounds__(256, 3) pack_kernel(PackParams P) {
+__global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
     constexpr int PPW = PACK_PPW;
     __shared__ int s_bad, s_route[N_ROUTES], s_maxn, s_maxm, s_malformed;
     __shared__ unsigned long long s_cells;
