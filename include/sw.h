@@ -95,10 +95,13 @@ typedef struct {
  * OR-ed with either) keeps linear-gap scorings (gap_open == gap_extend) on the
  * affine kernels instead of the two-state linear-gap kernels (PAPER.md:161-163:
  * the gap scores are free parameters; results are identical either way -- the
- * flag exists for comparison and testing).  Applies to every later call on
- * the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown mode bit.
+ * flag exists for comparison and testing).  Flag SW_MODE_TB_INT32 keeps every
+ * sw_traceback pair on the int32 path kernel instead of the s16x2 one (two DNA
+ * pairs per warp; identical paths -- comparison and testing).  Applies to every
+ * later call on the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown
+ * mode bit.
  */
-typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2 } sw_mode_t;
+typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2, SW_MODE_TB_INT32 = 4 } sw_mode_t;
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
 
 /*
@@ -142,10 +145,11 @@ sw_status_t sw_init(sw_handle_t* handle, int device);
  *   out               HOST struct of DEVICE pointers (see sw_result_t)
  *   stream            a cudaStream_t (NULL = legacy default stream)
  * Work is enqueued on `stream`; inputs and outputs must stay untouched until
- * it completes.  The call synchronises on `stream` twice (to read the payload
- * extents q/r_offsets[0], [n_pairs] and the per-batch length statistics that
- * size the workspace), so it returns after earlier work on `stream` is done
- * but before this batch's kernels finish.  Per-pair errors do not fail the
+ * it completes.  The call synchronises on `stream` once (to read the
+ * per-batch length statistics that size the launches; the first call of a
+ * handle, or one whose payload outgrows the handle's code buffers, also reads
+ * the payload extents q/r_offsets[0], [n_pairs] first), so it returns after
+ * earlier work on `stream` is done but before this batch's kernels finish.  Per-pair errors do not fail the
  * call: they appear as -1 sentinels and are counted by sw_batch_status.
  */
 sw_status_t sw_align_batch(sw_handle_t h,

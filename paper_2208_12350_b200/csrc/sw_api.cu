@@ -105,7 +105,7 @@ struct sw_context {
     // alignment paths (sw_traceback): per-warp direction words and stripe boundary rows
     DevBuf<uint32_t> tb_dir;
     DevBuf<int2> tb_bnd;
-    int32_t* d_tb = nullptr;   // [0] max a, [1] max b, [2] queue head, [3] internal errors; then int64 q0, r0
+    int32_t* d_tb = nullptr;   // [0] max a, [1] max b, [2] queue head, [3] internal errors; int64 q0, r0; [8] s16x2 queue head
     int32_t* h_tb = nullptr;   // pinned copy
     // asynchronous host-buffer entry point: double-buffered staging, copy-in / copy-out streams
     DevBuf<uint8_t> as_q[2], as_r[2];
@@ -619,7 +619,7 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
         cudaMalloc(&h->d_sink, 1024 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_hist, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_binbase, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
-        cudaMalloc(&h->d_tb, 8 * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->d_tb, 12 * sizeof(int32_t)) != cudaSuccess ||
         cudaMallocHost(&h->h_tb, 8 * sizeof(int32_t)) != cudaSuccess) {
         sw_free(h);
         return SW_ERR_OUT_OF_MEMORY;
@@ -818,7 +818,7 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
     if (st != SW_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     // 1. the batch's largest interval (sizes the per-warp scratch) and the offset bases
-    SW_CUDA(h, cudaMemsetAsync(h->d_tb, 0, 4 * sizeof(int32_t), s));
+    SW_CUDA(h, cudaMemsetAsync(h->d_tb, 0, 12 * sizeof(int32_t), s));
     int64_t* base = reinterpret_cast<int64_t*>(h->d_tb + 4);
     trace_extent_kernel<<<(int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 8), 256, 0, s>>>(
         *res, n_pairs, q_offsets, r_offsets, h->d_tb, base);
@@ -832,12 +832,15 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
     const int64_t dir_words = ns * (((int64_t)max_b + 31 + 31) & ~(int64_t)31) * 32;
     const int64_t bnd_len = (int64_t)max_b + 1;
     const int64_t budget_words = ((int64_t)4 << 30) / 4;
+    // DNA batches: the s16x2 kernel (two pairs per warp, two direction regions per warp) takes the
+    // pairs tb16_ok() admits, then the int32 kernel the rest
+    const bool use16 = sc.alphabet == SW_ALPHABET_DNA && !(h->mode & SW_MODE_TB_INT32);
     int64_t warps = std::min<int64_t>((int64_t)h->sm_count * 4 * occupancy_blocks((const void*)traceback_kernel, 128, 0),
-                                      std::max<int64_t>(4, budget_words / std::max<int64_t>(dir_words, 1)));
+                                      std::max<int64_t>(4, budget_words / std::max<int64_t>((use16 ? 2 : 1) * dir_words, 1)));
     warps = std::min<int64_t>(warps, std::max<int64_t>(4, n_pairs));
     warps = (warps + 3) / 4 * 4;
     {
-        sw_status_t e = ensure(h, h->tb_dir, (size_t)(warps * dir_words));
+        sw_status_t e = ensure(h, h->tb_dir, (size_t)(warps * dir_words * (use16 ? 2 : 1)));
         if (e != SW_OK) return e;
         e = ensure(h, h->tb_bnd, (size_t)(warps * bnd_len));
         if (e != SW_OK) return e;
@@ -846,7 +849,11 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
     T.queries = queries; T.q_off = q_offsets; T.refs = refs; T.r_off = r_offsets; T.n_pairs = n_pairs;
     T.q0 = q0; T.r0 = r0; T.res = *res; T.ops = ops; T.n_ops = n_ops; T.sc = sc;
     T.dir = h->tb_dir.p; T.dir_words = dir_words; T.bnd = h->tb_bnd.p; T.bnd_len = bnd_len;
-    T.counter = h->d_tb + 2; T.err = h->d_tb + 3;
+    T.counter = h->d_tb + 2; T.err = h->d_tb + 3; T.counter16 = h->d_tb + 8; T.skip16 = use16 ? 1 : 0;
+    if (use16) {
+        traceback16_kernel<<<(int)(warps / 4), 128, 0, s>>>(T);
+        SW_CUDA(h, cudaGetLastError());
+    }
     traceback_kernel<<<(int)(warps / 4), 128, 0, s>>>(T);
     SW_CUDA(h, cudaGetLastError());
     h->last_stream = s;
@@ -855,7 +862,8 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
 
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
-    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY)) return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
+    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32))
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
     h->mode = mode;
     return SW_OK;
 }

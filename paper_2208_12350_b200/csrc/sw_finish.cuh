@@ -44,8 +44,14 @@ __device__ __forceinline__ void decode_key(unsigned long long key, int& S, int& 
 // warp writes the pairs' reversed prefixes as one flat list of aligned 32-bit
 // words (every word = one PRMT of two aligned source words), so the loads of
 // all its pairs are in flight together.
-constexpr int FIN_PPW = 8;
-constexpr int FIN_FB = 4;   // words per lane loaded before any is stored
+#ifndef SW_FIN_PPW
+#define SW_FIN_PPW 8
+#endif
+#ifndef SW_FIN_FB
+#define SW_FIN_FB 4
+#endif
+constexpr int FIN_PPW = SW_FIN_PPW;
+constexpr int FIN_FB = SW_FIN_FB;   // words per lane loaded before any is stored
 
 __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     __shared__ int s_route[N_ROUTES];

@@ -574,3 +574,34 @@ def test_speculative_extents_grow_and_rerun():
         assert_parity(a.align(small), oracle_batch(small), small)
     finally:
         a.close()
+
+
+@pytest.mark.parametrize("which", ["mixed_eligibility", "c5_long"])
+def test_traceback_s16x2_and_int32_kernels_agree(aligner, which):
+    """DNA paths go to the s16x2 kernel (two pairs per warp) when every value fits 16 bits and to
+    the int32 kernel otherwise (tb16_ok); SW_MODE_TB_INT32 forces the int32 kernel.  Both must give
+    the oracle's paths; the mixed batch puts eligible and ineligible pairs in the same warp."""
+    rng = np.random.default_rng(23)
+    if which == "mixed_eligibility":
+        # gap_extend -30: long intervals exceed the 16-bit bound (2|o| + (a+b)|e| > 16000), short ones fit
+        pairs = []
+        for k in range(120):
+            n = int(rng.integers(5, 400)) if k % 3 else int(rng.integers(300, 420))
+            q = "".join(rng.choice(list("ACGT"), n))
+            mut = [c if rng.random() > 0.03 else str(rng.choice(list("ACGT"))) for c in q]
+            if k % 5 == 0:
+                mut.insert(len(mut) // 2, "ACG")
+            pairs.append((q, "".join(rng.choice(list("ACGT"), int(rng.integers(0, 40)))) + "".join(mut)))
+        b = synth.from_pairs(pairs, {"alphabet": "dna", "match": 5, "mismatch": -4, "gap_open": -40, "gap_extend": -30})
+    else:
+        b = synth.generate("c5", 0, 250)
+    exp = _oracle_paths(b)
+    got16 = aligner.traceback(b)
+    aligner.set_mode(sw.SW_MODE_TB_INT32)
+    try:
+        got32 = aligner.traceback(b)
+    finally:
+        aligner.set_mode(sw.SW_MODE_FULL)
+    for got in (got16, got32):
+        bad = [p for p in range(b.n_pairs) if got[p] != exp[p]]
+        assert not bad, f"{len(bad)} paths differ; first pair {bad[0]}: gpu={got[bad[0]]!r} oracle={exp[bad[0]]!r}"
