@@ -281,6 +281,7 @@ __device__ __forceinline__ uint32_t splat16(int v) { return ((uint32_t)v & 0xfff
 __global__ void __launch_bounds__(128) traceback16_kernel(const TraceParams P) {
     __shared__ uint8_t lut[256];
     __shared__ uint32_t tbuf[4][2][32][33];  // per warp and half: 32 steps x 32 lanes of direction words
+    __shared__ uint16_t selring[4][64];      // per warp: PRMT selector of columns j (index j & 63)
     for (int c = threadIdx.x; c < 256; c += blockDim.x) lut[c] = ascii_code(P.sc.alphabet, c);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -347,6 +348,16 @@ __global__ void __launch_bounds__(128) traceback16_kernel(const TraceParams P) {
             __syncwarp();
             for (int t = 0; t < steps; ++t) {
                 const int j = t - lane + 1;
+                if ((t & 31) == 0) {
+                    // selectors of columns t + 1 .. t + 32, one per lane (the ring keeps the previous
+                    // 32, which the lagging lanes still read): bytes s(q, r0c) sign-extended into
+                    // the low half, s(q, r1c) into the high half
+                    const int jj = t + 1 + lane;
+                    const uint32_t r0c = jj <= bb[0] ? lut[B0[jj - 1]] : 0u, r1c = jj <= bb[1] ? lut[B1[jj - 1]] : 0u;
+                    selring[wib][jj & 63] =
+                        (uint16_t)(r0c | ((r0c | 8u) << 4) | ((r1c + 4u) << 8) | (((r1c + 4u) | 8u) << 12));
+                    __syncwarp();
+                }
                 uint32_t upH = __shfl_up_sync(FULL, hoLast, 1);
                 uint32_t upF = __shfl_up_sync(FULL, fLast, 1);
                 if (lane == 0 && j >= 1 && j <= bmax) {
@@ -355,9 +366,7 @@ __global__ void __launch_bounds__(128) traceback16_kernel(const TraceParams P) {
                 }
                 uint32_t w0 = 0, w1 = 0;
                 if (j >= 1 && j <= bmax) {
-                    const uint32_t r0c = j <= bb[0] ? lut[B0[j - 1]] : 0u, r1c = j <= bb[1] ? lut[B1[j - 1]] : 0u;
-                    // bytes: s(q, r0c) sign-extended into the low half, s(q, r1c) into the high half
-                    const uint32_t sel = r0c | ((r0c | 8u) << 4) | ((r1c + 4u) << 8) | (((r1c + 4u) | 8u) << 12);
+                    const uint32_t sel = selring[wib][j & 63];
                     uint32_t hd = diagUp, hu = upH, F = upF;
 #pragma unroll
                     for (int r = 0; r < TB_K; ++r) {
