@@ -156,18 +156,34 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
     const int o = P.sc.gap_open, e = P.sc.gap_extend;
 
     for (;;) {
-        int p32 = 0;
-        if (lane == 0) p32 = atomicAdd(P.counter, 1);
-        const int64_t p = __shfl_sync(FULL, p32, 0);
-        if (p >= P.n_pairs) break;
-        const int S = P.res.score[p];
-        if (S <= 0) {
-            if (lane == 0) P.n_ops[p] = S == 0 ? 0 : -1;
-            continue;
+      // 32 pairs per queue step: the lanes sort out S <= 0 pairs and the pairs the s16x2 kernel
+      // took, then the warp aligns the rest one by one
+      // (one pair per step when there is no s16x2 kernel: every pair is work, keep the warps busy)
+      const int grab = P.skip16 ? 32 : 1;
+      int b32 = 0;
+      if (lane == 0) b32 = atomicAdd(P.counter, grab);
+      const int64_t pbase = __shfl_sync(FULL, b32, 0);
+      if (pbase >= P.n_pairs) break;
+      bool need = false;
+      {
+        const int64_t pl = pbase + lane;
+        if (lane < grab && pl < P.n_pairs) {
+            const int Sl = P.res.score[pl];
+            if (Sl <= 0) {
+                P.n_ops[pl] = Sl == 0 ? 0 : -1;
+            } else {
+                const int al = P.res.q_end[pl] - P.res.q_start[pl] + 1, bl = P.res.r_end[pl] - P.res.r_start[pl] + 1;
+                need = !(P.skip16 && tb16_ok(P.sc, Sl, al, bl));  // else done by traceback16_kernel
+            }
         }
+      }
+      uint32_t todo = __ballot_sync(FULL, need);
+      while (todo) {
+        const int64_t p = pbase + (__ffs(todo) - 1);
+        todo &= todo - 1;
+        const int S = P.res.score[p];
         const int qs = P.res.q_start[p], qe = P.res.q_end[p], rs = P.res.r_start[p], re = P.res.r_end[p];
         const int a = qe - qs + 1, b = re - rs + 1;
-        if (P.skip16 && tb16_ok(P.sc, S, a, b)) continue;  // done by traceback16_kernel
         const int ns = (a + TB_ROWS - 1) / TB_ROWS;
         const int steps = b + 31;           // column j (1-based) of lane L at step t: j = t - L + 1
         const int steps_pad = (steps + 31) & ~31;
@@ -261,6 +277,7 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         }
         if (lane == 0) P.n_ops[p] = len;
         __syncwarp();
+      }
     }
 }
 
