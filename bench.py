@@ -26,6 +26,7 @@ cores) on a bounded sample of the same workload (rank 0 only).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -429,6 +430,40 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                               "ops_total": int(n_ops[:batch.n_pairs].clamp(min=0).sum().item())}
 
     if rank == 0 and not args.no_extra:
+        # linear gaps (gap_open == gap_extend: the two-state kernels), same shard
+        lin = {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -4, "gap_extend": -4}
+        out_x = a.alloc_out(batch.n_pairs)  # keep `out` (the headline run's results) for the parity leg
+        tl, sl = time_device_steps(a, q, qo, r, ro, lin, out_x, 5, 2, flush_buf, torch)
+        med = float(np.median(tl))
+        extra["linear_gap"] = {"workload": "rank-0 shard, DNA 3/-3, gap -4 per residue (two-state kernels)",
+                               "ms": round(med, 3), "gcups": round(cells / med / 1e6, 1),
+                               "fwd_kernel_gcups": round(cells / float(np.median([x["fwd"] for x in sl])) / 1e6, 1)}
+        # one query against the shard's references (sw_align_query_db)
+        n0 = int(batch.q_offsets[1] - batch.q_offsets[0])
+        qd = q[:max(n0, 1)].clone()
+        qcells = float(n0) * float(batch.r_offsets[-1] - batch.r_offsets[0])
+        res = sw.sw_result_t(*[out_x[i].data_ptr() for i in range(5)])
+        sc_db = sw.make_scoring(batch.scoring)
+        lib_ = sw.load()
+        tq = []
+        for k in range(7):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            flush_buf.zero_()
+            e0.record()
+            stq = lib_.sw_align_query_db(ctypes.c_void_p(a.handle), ctypes.c_void_p(qd.data_ptr()), n0,
+                                         ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(ro.data_ptr()), batch.n_pairs,
+                                         ctypes.byref(sc_db), ctypes.byref(res),
+                                         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            e1.record()
+            e1.synchronize()
+            if stq != sw.SW_OK:
+                raise RuntimeError(f"sw_align_query_db: {sw.status_string(stq)}")
+            if k >= 2:
+                tq.append(e0.elapsed_time(e1))
+        med = float(np.median(tq))
+        extra["query_db"] = {"workload": f"one {n0}-bp query vs the shard's {batch.n_pairs} references",
+                             "ms": round(med, 3), "gcups": round(qcells / med / 1e6, 1)}
         extra["simcov"] = simcov_extra(torch, args.no_cpu_baseline)
 
     cpu = None
