@@ -67,6 +67,9 @@
 #ifndef SW_SKEW2
 #define SW_SKEW2 0         // 1: forward TAG sweep with a two-column skew per lane (sweep_skew2; measured slower)
 #endif
+#ifndef SW_PRED_IMPROVE
+#define SW_PRED_IMPROVE 0     // non-TAG forward: record running-max improvements branch-free
+#endif
 #ifndef SW_REV_BODY_BLOCKS
 #define SW_REV_BODY_BLOCKS 1  // reverse pass: the stop column is re-checked after every block either way
 #endif
@@ -191,6 +194,22 @@ __device__ __forceinline__ void sv_store_arr(uint32_t addr, const uint32_t (&v)[
 #pragma unroll
     for (int r = 0; r < K; ++r) q[r] = v[r];
     sv_store<K>(addr, q);
+}
+
+// sv_store under a predicate (no branch): the stores issue always, write only where `cond` != 0.
+template <int K>
+__device__ __forceinline__ void sv_store_if(uint32_t addr, const uint32_t (&v)[K], uint32_t cond) {
+#pragma unroll
+    for (int w = 0; w < K / 4; ++w)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
+                     :: "r"(addr + 16 * w), "r"(v[4 * w]), "r"(v[4 * w + 1]), "r"(v[4 * w + 2]), "r"(v[4 * w + 3]),
+                     "r"(cond) : "memory");
+    if (K % 4 >= 2)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.shared.v2.u32 [%0], {%1, %2};\n\t}"
+                     :: "r"(addr + 16 * (K / 4)), "r"(v[4 * (K / 4)]), "r"(v[4 * (K / 4) + 1]), "r"(cond) : "memory");
+    if (K % 4 == 1 || K % 4 == 3)
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}"
+                     :: "r"(addr + 16 * (K / 4) + (K % 4 == 3 ? 8u : 0u)), "r"(v[K - 1]), "r"(cond) : "memory");
 }
 
 // First row r of the saved column whose half h equals `target` (an HO value).
@@ -522,6 +541,17 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     }
                 } else if (SW_ABLATE & 1) {
                     best = nb;  // timing ablation only: no improvement bookkeeping
+                } else if (SW_PRED_IMPROVE && SW_XFORM) {
+                    // branch-free: per half, predicated stores of the column's values and a
+                    // predicated column update where the half's running max improved
+                    const uint32_t d = nb ^ best;
+#pragma unroll
+                    for (int h = 0; h < NH; ++h) {
+                        const uint32_t dh = NH == 1 ? d : (h ? d >> 16 : d & 0xffffu);
+                        sv_store_if<K>(sv[h], H, dh);
+                        bc[h] = dh ? t - L : bc[h];
+                    }
+                    best = nb;
                 } else if (nb != best) {
                     const uint32_t d = nb ^ best;
 #pragma unroll
