@@ -241,6 +241,88 @@ __global__ void __launch_bounds__(NW * 32, SIMCOV_TB_MINB) diffuse_tblock_kernel
     }
 }
 
+// The same K-step tile computation as a persistent kernel: each CTA walks tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ...; while it computes one tile in registers, cp.async copies the next
+// tile's rows (each thread its own 16-byte words) into a shared staging area, so HBM latency is
+// paid once per CTA instead of once per tile.
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gptr, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(saddr), "l"(gptr), "r"(valid ? 16 : 0) : "memory");
+}
+
+template <int K, int NW, int RPW>
+__global__ void __launch_bounds__(NW * 32, SIMCOV_TB_MINB) diffuse_tblock_pipe_kernel(
+    const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int64_t pitch, int64_t fstride, int H, int W,
+    int n_fields, int ntx, int nty, const __grid_constant__ Rates rates) {
+    constexpr int HALO = K <= 4 ? 4 : 8;
+    constexpr int OUTC = 128 - 2 * HALO;
+    constexpr int TH = NW * RPW - 2 * K;
+    constexpr int NT = NW * 32;
+    extern __shared__ uint4 stage[];           // [RPW][NT]: thread-contiguous per row
+    __shared__ uint4 pub[2 * 2 * NW * 32];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int64_t total = (int64_t)ntx * nty * n_fields;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage);
+    auto prefetch = [&](int64_t tile) {
+        const int tx = (int)(tile % ntx);
+        const int64_t rest = tile / ntx;
+        const int ty = (int)(rest % nty), field = (int)(rest / nty);
+        const int64_t tx0 = (int64_t)tx * OUTC + kColPad - HALO;
+        const int64_t pc = tx0 + lane * 4;
+        const bool cin = pc >= 0 && pc + 4 <= pitch;
+        const int gy0 = ty * TH - K + w * RPW;
+        const uint32_t* s = src + (int64_t)field * fstride + (cin ? pc : 0);
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+            const int pr = gy0 + r + 1;
+            const bool ok = cin && pr >= 0 && pr < H + 2;
+            cp_async16(sbase + (uint32_t)((r * NT + tid) * 16), ok ? s + (int64_t)pr * pitch : src, ok);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int64_t tile = blockIdx.x;
+    if (tile >= total) return;
+    prefetch(tile);
+    for (; tile < total; tile += gridDim.x) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        uint4 v[RPW];
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) v[r] = stage[r * NT + tid];
+        __syncthreads();  // every thread's staged words are in registers before the next copy lands
+        if (tile + gridDim.x < total) prefetch(tile + gridDim.x);
+        const int tx = (int)(tile % ntx);
+        const int64_t rest = tile / ntx;
+        const int ty = (int)(rest % nty), field = (int)(rest / nty);
+        const uint32_t a = rates.a[field];
+        const int64_t tx0 = (int64_t)tx * OUTC + kColPad - HALO;
+        const int ty0 = ty * TH;
+        const int gx = (int)tx0 - (int)kColPad + lane * 4;
+        const int64_t pc = tx0 + lane * 4;
+        const int gy0 = ty0 - K + w * RPW;
+        const bool edge = ty0 - K < 0 || ty0 - K + NW * RPW > H || (int)tx0 - (int)kColPad < 0 ||
+                          (int)tx0 - (int)kColPad + 128 > W;
+        if (edge) {
+            const uint4 cm = make_uint4(gx >= 0 && gx < W ? ~0u : 0u, gx + 1 >= 0 && gx + 1 < W ? ~0u : 0u,
+                                        gx + 2 >= 0 && gx + 2 < W ? ~0u : 0u, gx + 3 >= 0 && gx + 3 < W ? ~0u : 0u);
+            uint32_t rmask = 0;
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) rmask |= (gy0 + r >= 0 && gy0 + r < H) ? (1u << r) : 0u;
+            tblock_run<K, NW, RPW, true>(v, pub, w, lane, a, cm, rmask);
+        } else {
+            tblock_run<K, NW, RPW, false>(v, pub, w, lane, a, make_uint4(0, 0, 0, 0), 0u);
+        }
+        if (!(lane < HALO / 4 || lane >= 32 - HALO / 4 || gx >= W)) {
+            uint32_t* d = dst + (int64_t)field * fstride + pc;
+#pragma unroll
+            for (int r = 0; r < RPW; ++r) {
+                const int row = w * RPW + r, gy = gy0 + r;
+                if (row >= K && row < K + TH && gy < H) store4(d + (int64_t)(gy + 1) * pitch, v[r], W - gx);
+            }
+        }
+        __syncthreads();  // the exchange buffer `pub` is reused by the next tile's first step
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // Zero every padding word of n_fields padded fields: warp per padded row.
 __global__ void zero_ring_kernel(uint32_t* __restrict__ g, int64_t pitch, int64_t fstride, int H, int W,
@@ -323,12 +405,39 @@ sw_status_t launch_step(const uint32_t* src, uint32_t* dst, int64_t pitch, int64
     return check_launch("diffuse_step_kernel");
 }
 
+#ifndef SIMCOV_TB_PIPE
+#define SIMCOV_TB_PIPE 0  // persistent CTAs with a cp.async-prefetched next tile: measured slower
+#endif
+
+template <int K>
+sw_status_t launch_tblock_pipe_k(const uint32_t* src, uint32_t* dst, int64_t pitch, int64_t fstride, int H, int W,
+                                 int n_fields, const Rates& rates, cudaStream_t st) {
+    constexpr int HALO = K <= 4 ? 4 : 8, TH = kTbWarps * kTbRowsPerWarp - 2 * K;
+    const int ntx = (W + 128 - 2 * HALO - 1) / (128 - 2 * HALO), nty = (H + TH - 1) / TH;
+    const size_t smem = (size_t)kTbRowsPerWarp * kTbWarps * 32 * 16;
+    auto kern = diffuse_tblock_pipe_kernel<K, kTbWarps, kTbRowsPerWarp>;
+    static int occ = -1;  // per process: CTAs per SM of this instantiation
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (occ < 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTbWarps * 32, smem) != cudaSuccess || occ < 1) occ = 1;
+    }
+    const int64_t total = (int64_t)ntx * nty * n_fields;
+    const int blocks = (int)std::min<int64_t>(total, (int64_t)sms * occ);
+    kern<<<blocks, kTbWarps * 32, smem, st>>>(src, dst, pitch, fstride, H, W, n_fields, ntx, nty, rates);
+    ++g_launches;
+    return check_launch("diffuse_tblock_pipe_kernel");
+}
+
 template <int K>
 sw_status_t launch_tblock_k(const uint32_t* src, uint32_t* dst, int64_t pitch, int64_t fstride, int H, int W,
                             int n_fields, const Rates& rates, cudaStream_t st) {
     constexpr int HALO = K <= 4 ? 4 : 8, TH = kTbWarps * kTbRowsPerWarp - 2 * K;
     dim3 grid((unsigned)((W + 128 - 2 * HALO - 1) / (128 - 2 * HALO)), (unsigned)((H + TH - 1) / TH),
               (unsigned)n_fields);
+    if (SIMCOV_TB_PIPE) return launch_tblock_pipe_k<K>(src, dst, pitch, fstride, H, W, n_fields, rates, st);
     if (grid.y > 65535u) return fail(SW_ERR_INVALID_ARGUMENT, "grid too tall for the temporal-blocking schedule");
     diffuse_tblock_kernel<K, kTbWarps, kTbRowsPerWarp><<<grid, kTbWarps * 32, 0, st>>>(src, dst, pitch, fstride, H,
                                                                                         W, rates);
