@@ -1,0 +1,85 @@
+"""Randomised parity soak (development tool): random batches under random valid scorings, every
+field and every alignment path compared with the oracle.  python tools/soak.py [seconds]"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_2208_12350_b200 import sw, synth  # noqa: E402
+
+FIELDS = ("score", "q_end", "r_end", "q_start", "r_start")
+
+
+def random_scoring(rng):
+    if rng.random() < 0.3:
+        o = -int(rng.integers(1, 20))
+        e = o if rng.random() < 0.3 else int(rng.integers(o, 1))
+        return {"alphabet": "protein", "match": 0, "mismatch": 0, "gap_open": o, "gap_extend": e}
+    m = int(rng.integers(1, 12))
+    x = int(rng.integers(-12, m))
+    o = -int(rng.integers(1, 40))
+    e = o if rng.random() < 0.3 else int(rng.integers(o, 1))
+    return {"alphabet": "dna", "match": m, "mismatch": x, "gap_open": o, "gap_extend": e}
+
+
+def batch(rng, sc):
+    alpha = "ARNDCQEGHILKMFPSTWYV" if sc["alphabet"] == "protein" else ("AC" if rng.random() < 0.3 else "ACGT")
+    pairs = []
+    for _ in range(int(rng.integers(1, 400))):
+        n = int(rng.integers(0, 420)) if rng.random() < 0.9 else int(rng.integers(400, 1300))
+        q = "".join(rng.choice(list(alpha), n))
+        if rng.random() < 0.6 and n:
+            mut = [c if rng.random() > 0.1 else str(rng.choice(list(alpha))) for c in q]
+            r = "".join(rng.choice(list(alpha), int(rng.integers(0, 60)))) + "".join(mut)
+        else:
+            r = "".join(rng.choice(list(alpha), int(rng.integers(0, 420))))
+        if rng.random() < 0.02:
+            q = q.lower()
+        pairs.append((q, r))
+    return synth.from_pairs(pairs, sc)
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+    rng = np.random.default_rng(int(time.time()) & 0xffff)
+    a = sw.Aligner(0)
+    t0 = time.time()
+    nb = npairs = 0
+    try:
+        while time.time() - t0 < budget:
+            sc = random_scoring(rng)
+            b = batch(rng, sc)
+            got = a.align(b)
+            exp = oracle.align_batch(b.queries, b.q_offsets, b.refs, b.r_offsets, b.scoring)
+            for f in FIELDS:
+                bad = np.nonzero(got[f] != exp[f])[0]
+                if bad.size:
+                    p = int(bad[0])
+                    print("MISMATCH", f, sc, p, b.pair(p), [int(got[k][p]) for k in FIELDS],
+                          [int(exp[k][p]) for k in FIELDS], flush=True)
+                    return 1
+            if rng.random() < 0.5:
+                paths = a.traceback(b)
+                for p in range(b.n_pairs):
+                    q, r = b.pair(p)
+                    res = tuple(int(exp[k][p]) for k in FIELDS)
+                    want = oracle.traceback(q, r, b.scoring, res) if res[0] >= 0 else None
+                    if paths[p] != want:
+                        print("PATH MISMATCH", sc, p, (q, r), paths[p], want, flush=True)
+                        return 1
+            nb += 1
+            npairs += b.n_pairs
+    finally:
+        a.close()
+    print(f"soak ok: {nb} batches, {npairs} pairs, {time.time() - t0:.0f} s", flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
