@@ -155,32 +155,8 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
     int2* bnd = P.bnd + gwarp * P.bnd_len;
     const int o = P.sc.gap_open, e = P.sc.gap_extend;
 
-    for (;;) {
-      // 32 pairs per queue step: the lanes sort out S <= 0 pairs and the pairs the s16x2 kernel
-      // took, then the warp aligns the rest one by one
-      // (one pair per step when there is no s16x2 kernel: every pair is work, keep the warps busy)
-      const int grab = P.skip16 ? 32 : 1;
-      int b32 = 0;
-      if (lane == 0) b32 = atomicAdd(P.counter, grab);
-      const int64_t pbase = __shfl_sync(FULL, b32, 0);
-      if (pbase >= P.n_pairs) break;
-      bool need = false;
-      {
-        const int64_t pl = pbase + lane;
-        if (lane < grab && pl < P.n_pairs) {
-            const int Sl = P.res.score[pl];
-            if (Sl <= 0) {
-                P.n_ops[pl] = Sl == 0 ? 0 : -1;
-            } else {
-                const int al = P.res.q_end[pl] - P.res.q_start[pl] + 1, bl = P.res.r_end[pl] - P.res.r_start[pl] + 1;
-                need = !(P.skip16 && tb16_ok(P.sc, Sl, al, bl));  // else done by traceback16_kernel
-            }
-        }
-      }
-      uint32_t todo = __ballot_sync(FULL, need);
-      while (todo) {
-        const int64_t p = pbase + (__ffs(todo) - 1);
-        todo &= todo - 1;
+    // one pair, warp-cooperative: recurrence + direction bits, walk, reversal
+    auto one_pair = [&](const int64_t p) {
         const int S = P.res.score[p];
         const int qs = P.res.q_start[p], qe = P.res.q_end[p], rs = P.res.r_start[p], re = P.res.r_end[p];
         const int a = qe - qs + 1, b = re - rs + 1;
@@ -189,7 +165,7 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         const int steps_pad = (steps + 31) & ~31;
         if ((int64_t)ns * steps_pad * 32 > P.dir_words || b + 1 > P.bnd_len) {
             if (lane == 0) { P.n_ops[p] = -1; atomicAdd(P.err, 1); }
-            continue;
+            return;
         }
         const uint8_t* A = P.queries + P.q_off[p] + qs;
         const uint8_t* B = P.refs + P.r_off[p] + rs;
@@ -277,7 +253,29 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         }
         if (lane == 0) P.n_ops[p] = len;
         __syncwarp();
-      }
+    };
+
+    for (;;) {
+        // 32 pairs per queue step: the lanes sort out S <= 0 pairs and the pairs the s16x2 kernel
+        // took, then the warp aligns the rest one by one (one pair per step when there is no
+        // s16x2 kernel: every pair is work, keep the warps busy)
+        const int grab = P.skip16 ? 32 : 1;
+        int b32 = 0;
+        if (lane == 0) b32 = atomicAdd(P.counter, grab);
+        const int64_t pbase = __shfl_sync(FULL, b32, 0);
+        if (pbase >= P.n_pairs) break;
+        bool need = false;
+        const int64_t pl = pbase + lane;
+        if (lane < grab && pl < P.n_pairs) {
+            const int Sl = P.res.score[pl];
+            if (Sl <= 0) {
+                P.n_ops[pl] = Sl == 0 ? 0 : -1;
+            } else {
+                const int al = P.res.q_end[pl] - P.res.q_start[pl] + 1, bl = P.res.r_end[pl] - P.res.r_start[pl] + 1;
+                need = !(P.skip16 && tb16_ok(P.sc, Sl, al, bl));  // else done by traceback16_kernel
+            }
+        }
+        for (uint32_t todo = __ballot_sync(FULL, need); todo; todo &= todo - 1) one_pair(pbase + (__ffs(todo) - 1));
     }
 }
 
