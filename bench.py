@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-extra", action="store_true", help="skip the protein / C1 side measurements")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the side measurements (other configs, modes, paths, diffusion); N > 1 runs skip them")
     ap.add_argument("--no-c5", action="store_true", help="skip the c5 (400k mixed pairs, ~1 min to generate) extra")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -391,7 +392,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     all_cells = float(cells_t[0].item())
 
     extra = {}
-    if rank == 0 and not args.no_extra:
+    if rank == 0 and world == 1 and not args.no_extra:
         for key in ("c3", "c1") + (() if args.no_c5 else ("c5",)):
             bx = synth.generate(key)
             qx, qox, rx, rox = a.to_device(bx)
@@ -404,7 +405,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                           "ms": round(med, 3), "fwd_kernel_gcups": round(bx.cells() / float(np.median([x["fwd"] for x in sx])) / 1e6, 1),
                           "stage_ms": {k: round(float(np.median([x[k] for x in sx])), 4) for k in sx[0]}}
 
-    if rank == 0 and not args.no_extra:
+    if rank == 0 and world == 1 and not args.no_extra:
         # forward pass only (SW_MODE_END_ONLY: score, q_end, r_end), the same shard
         a.set_mode(sw.SW_MODE_END_ONLY)
         te, se = time_device_steps(a, q, qo, r, ro, batch.scoring, out, 5, 2, flush_buf, torch)
@@ -432,7 +433,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                               "pairs_per_s": round(batch.n_pairs / med * 1e3, 1),
                               "ops_total": int(n_ops[:batch.n_pairs].clamp(min=0).sum().item())}
 
-    if rank == 0 and not args.no_extra:
+    if rank == 0 and world == 1 and not args.no_extra:
         # linear gaps (gap_open == gap_extend: the two-state kernels), same shard
         lin = {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -4, "gap_extend": -4}
         out_x = a.alloc_out(batch.n_pairs)  # keep `out` (the headline run's results) for the parity leg
@@ -471,7 +472,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     cpu = None
     parity = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sub, o, dt, cores = oracle_sample(batch)
         cpu = {"value": round(sub.cells() / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
                "sample": f"first {sub.n_pairs} pairs of the rank-0 shard ({sub.cells():.3e} forward cells), "
