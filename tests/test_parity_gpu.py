@@ -115,6 +115,20 @@ def test_c2_full_size_sampled(aligner):
     assert np.all(got["score"] > 0)
 
 
+def test_c3_full_size_sampled(aligner):
+    """C3 (50k protein pairs, BLOSUM62, lengths up to 1,024) at its full size in one call; 300
+    sampled pairs vs the oracle, and every pair's start/end consistent with its score."""
+    b = synth.generate("c3")
+    got = aligner.align(b)
+    rng = np.random.default_rng(3)
+    idx = np.sort(rng.choice(b.n_pairs, size=300, replace=False))
+    sub = b.subset(idx)
+    assert_parity({f: got[f][idx] for f in FIELDS}, oracle_batch(sub), sub)
+    pos = got["score"] > 0
+    assert np.all(got["q_start"][pos] <= got["q_end"][pos]) and np.all(got["r_start"][pos] <= got["r_end"][pos])
+    assert np.all(got["q_end"][~pos] == -1)
+
+
 def test_c4_per_gpu_share_sampled(aligner):
     """C4 (4M pairs) at 8 GPUs gives each GPU 500k pairs: one such call, 300 sampled pairs vs the oracle."""
     b = synth.generate("c4", 3_500_000, 4_000_000)
