@@ -13,8 +13,9 @@
 // What is B200-specific is the rest:
 // * HBM-bound (8 B of algorithmic traffic per cell and step, one read + one
 //   write): 16-byte vector loads and stores, one warp per 128-column strip that
-//   marches down R rows keeping the rows above and below in registers (each
-//   word is loaded once), left/right neighbour shares by __shfl (only the two
+//   marches down R = 4 rows keeping the rows above and below in registers (short
+//   chunks: many warps in flight beat the re-read of the chunk's boundary rows,
+//   which L2 serves), left/right neighbour shares by __shfl (only the two
 //   strip-edge lanes load a scalar from the padding or the next strip);
 // * temporal blocking (k <= 8 steps per launch, the default schedule): a CTA of 8 warps
 //   loads a 128-word x 160-row tile straight into registers (20 rows per warp), runs k
@@ -391,7 +392,10 @@ sw_status_t check_layout(const void* p, int64_t H, int64_t W, int32_t n_fields, 
     return SW_OK;
 }
 
-constexpr int kStepRows = 16;
+#ifndef SIMCOV_STEP_ROWS
+#define SIMCOV_STEP_ROWS 4
+#endif
+constexpr int kStepRows = SIMCOV_STEP_ROWS;  // rows per warp of the one-step kernel
 
 sw_status_t launch_step(const uint32_t* src, uint32_t* dst, int64_t pitch, int64_t fstride, int H, int W,
                         int n_fields, const Rates& rates, cudaStream_t st) {
