@@ -95,8 +95,9 @@ sw_status_t simcov_diffuse(uint32_t* grid, uint32_t* scratch, int64_t H, int64_t
 
 /* Selects the kernel schedule for later simcov_diffuse calls of this process
  * (measurement and testing; results are identical):
- *   0 = auto (default), 1 = one step per launch, k >= 2 = up to k steps per
- *   launch through shared memory (temporal blocking), k <= SIMCOV_MAX_TBLOCK.
+ *   0 = auto (default: up to 8 steps per launch), 1 = one step per launch,
+ *   k >= 2 = up to k steps per launch (temporal blocking: a tile held in
+ *   registers for k steps), k <= SIMCOV_MAX_TBLOCK.
  * Errors: SW_ERR_INVALID_ARGUMENT for k outside [0, SIMCOV_MAX_TBLOCK]. */
 #define SIMCOV_MAX_TBLOCK 8
 sw_status_t simcov_set_schedule(int32_t steps_per_launch);
