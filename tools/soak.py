@@ -45,8 +45,39 @@ def batch(rng, sc):
     return synth.from_pairs(pairs, sc)
 
 
+def soak_diffusion(rng, budget):
+    """Random grids / rates / step counts / schedules of simcov_diffuse vs oracle/diffusion.py."""
+    from oracle import diffusion as D
+    from paper_2208_12350_b200 import simcov
+    t0 = time.time()
+    n = 0
+    while time.time() - t0 < budget:
+        H, W = int(rng.integers(1, 700)), int(rng.integers(1, 700))
+        nf = int(rng.integers(1, 4))
+        fields = synth.simcov_dense(int(rng.integers(0, 1 << 30)), H, W, nf, high=1 << int(rng.integers(8, 31)))
+        rates = [int(rng.integers(0, simcov.SIMCOV_MAX_RATE + 1)) for _ in range(nf)]
+        steps = int(rng.integers(0, 20))
+        sch = int(rng.choice([0, 1, 2, 3, 4, 5, 6, 7, 8]))
+        g = simcov.Grid(H, W, nf)
+        g.upload(fields)
+        simcov.simcov_set_schedule(sch)
+        g.diffuse(rates, steps)
+        got = g.download()
+        exp = D.diffuse(fields, rates, steps)
+        for f in range(nf):
+            if not np.array_equal(got[f], exp[f]):
+                print("DIFFUSION MISMATCH", H, W, nf, rates, steps, sch, flush=True)
+                return 1
+        n += 1
+    simcov.simcov_set_schedule(0)
+    print(f"diffusion soak ok: {n} random grids", flush=True)
+    return 0
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+    if len(sys.argv) > 2 and sys.argv[2] == "diffusion":
+        return soak_diffusion(np.random.default_rng(int(time.time()) & 0xffff), budget)
     rng = np.random.default_rng(int(time.time()) & 0xffff)
     a = sw.Aligner(0)
     t0 = time.time()
