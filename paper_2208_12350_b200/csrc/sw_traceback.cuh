@@ -157,7 +157,6 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
 
     // one pair, warp-cooperative: recurrence + direction bits, walk, reversal
     auto one_pair = [&](const int64_t p) {
-        const int S = P.res.score[p];
         const int qs = P.res.q_start[p], qe = P.res.q_end[p], rs = P.res.r_start[p], re = P.res.r_end[p];
         const int a = qe - qs + 1, b = re - rs + 1;
         const int ns = (a + TB_ROWS - 1) / TB_ROWS;

@@ -262,7 +262,6 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 
     Quads<K> HO;   // H of the lane's rows at the previous column (plain, >= 0)
     uint32_t E[K]; // Eb = E - o of the lane's rows at the previous column (>= 0)
-#pragma unroll
     const uint32_t o2s = T::splat(o);      // gap_open in every half
     // XF: HO holds R = H + o (column -1: H = 0), E holds max(E, 0); else HO holds H, E holds E - o
     const uint32_t R0 = SW_XFORM ? o2s : 0u;
@@ -525,7 +524,6 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                         for (int h = 0; h < NH; ++h) {
                             if (((x >> (16 * h)) & (NH == 1 ? 0xffffffffu : 0xffffu)) == 0u && h_pid[h] >= 0) {
                                 int rr = 0;
-#pragma unroll
                                 // whole-word compare under the half's mask (no 16-bit extraction, which
                                 // makes ptxas split the row values into 16-bit pieces in the hot path)
                                 const uint32_t tw = T::splat(h_tgt[h]);
