@@ -78,7 +78,9 @@ def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
     if len(sys.argv) > 2 and sys.argv[2] == "diffusion":
         return soak_diffusion(np.random.default_rng(int(time.time()) & 0xffff), budget)
-    rng = np.random.default_rng(int(time.time()) & 0xffff)
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else int(time.time() * 1000) & 0xffffffff
+    print(f"soak seed {seed}", flush=True)
+    rng = np.random.default_rng(seed)
     a = sw.Aligner(0)
     t0 = time.time()
     nb = npairs = 0
@@ -103,6 +105,10 @@ def main():
                     want = oracle.traceback(q, r, b.scoring, res) if res[0] >= 0 else None
                     if paths[p] != want:
                         print("PATH MISMATCH", sc, p, (q, r), paths[p], want, flush=True)
+                        np.savez("gpurun_out/soak_fail.npz", queries=b.queries, q_offsets=b.q_offsets, refs=b.refs,
+                                 r_offsets=b.r_offsets, pair=p, batch_index=nb)
+                        import json as _json
+                        _json.dump(sc, open("gpurun_out/soak_fail_scoring.json", "w"))
                         return 1
             nb += 1
             npairs += b.n_pairs
