@@ -97,11 +97,17 @@ typedef struct {
  * the gap scores are free parameters; results are identical either way -- the
  * flag exists for comparison and testing).  Flag SW_MODE_TB_INT32 keeps every
  * sw_traceback pair on the int32 path kernel instead of the s16x2 one (two DNA
- * pairs per warp; identical paths -- comparison and testing).  Applies to every
- * later call on the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown
- * mode bit.
+ * pairs per warp; identical paths -- comparison and testing).  Flag
+ * SW_MODE_POISON (debugging and tests) makes every later call first fill the
+ * caller's output arrays and the handle's internal workspace (stripe hand-off
+ * rows, work lists, reverse-pass metadata, path scratch) with poison bytes
+ * (0x7f / 0xff), so any value a call reads or returns without having written
+ * it in that call shows up as a wrong result instead of a stale plausible
+ * one; results are unchanged, calls are slower.  Applies to every later call
+ * on the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown mode bit.
  */
-typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2, SW_MODE_TB_INT32 = 4 } sw_mode_t;
+typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2, SW_MODE_TB_INT32 = 4,
+               SW_MODE_POISON = 8 } sw_mode_t;
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
 
 /*

@@ -105,8 +105,9 @@ struct sw_context {
     // alignment paths (sw_traceback): per-warp direction words and stripe boundary rows
     DevBuf<uint32_t> tb_dir;
     DevBuf<int2> tb_bnd;
-    int32_t* d_tb = nullptr;   // [0] max a, [1] max b, [2] queue head, [3] internal errors; int64 q0, r0; [8] s16x2 queue head
+    int32_t* d_tb = nullptr;   // [0] max a, [1] max b, [2] queue head, [3] internal errors; int64 q0, r0; [8] s16x2 queue head; [9] bad intervals
     int32_t* h_tb = nullptr;   // pinned copy
+    bool tb_pending = false;   // a traceback ran since the last sw_batch_status: read its error count
     // asynchronous host-buffer entry point: double-buffered staging, copy-in / copy-out streams
     DevBuf<uint8_t> as_q[2], as_r[2];
     DevBuf<int64_t> as_qo[2], as_ro[2];
@@ -174,6 +175,11 @@ template <class T>
 void release(DevBuf<T>& b) {
     if (b.p) cudaFree(b.p);
     b.p = nullptr; b.cap = 0;
+}
+
+// SW_MODE_POISON helper: p[0 .. n) = v.
+__global__ void fill_u32_kernel(uint32_t* p, size_t n, uint32_t v) {
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) p[k] = v;
 }
 
 // Scoring preconditions (reading R3) and the s16x2 routing condition.
@@ -386,6 +392,19 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     const bool timing = h->timing && !hp;
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[0], s));
 
+    // debugging (SW_MODE_POISON): whatever this call does not write reads back as poison
+    if (h->mode & SW_MODE_POISON) {
+        int32_t* fields[5] = {out->score, out->q_end, out->r_end, out->q_start, out->r_start};
+        for (int k = 0; k < (end_only ? 3 : 5); ++k)
+            SW_CUDA(h, cudaMemsetAsync(fields[k] + lo, 0x7f, (size_t)(hi - lo) * 4, s));
+        SW_CUDA(h, cudaMemsetAsync(h->order.p + lo, 0xff, (size_t)(hi - lo) * 4, s));
+        SW_CUDA(h, cudaMemsetAsync(h->order_rev.p + lo, 0xff, (size_t)(hi - lo) * 4, s));
+        SW_CUDA(h, cudaMemsetAsync(h->nlen_rev.p + lo, 0x7f, (size_t)(hi - lo) * 4, s));
+        SW_CUDA(h, cudaMemsetAsync(h->mlen_rev.p + lo, 0x7f, (size_t)(hi - lo) * 4, s));
+        SW_CUDA(h, cudaMemsetAsync(h->target.p + lo, 0x7f, (size_t)(hi - lo) * 4, s));
+        SW_CUDA(h, cudaMemsetAsync(h->keys_rev.p + lo, 0x7f, (size_t)(hi - lo) * 8, s));
+    }
+
     // 3. pack
     if (!hp) SW_CUDA(h, cudaMemsetAsync(h->d_stats, 0, N_SLOTS * sizeof(BatchStats), s));  // all slots' totals
     else if (hp->reset_cumulative) SW_CUDA(h, cudaMemsetAsync(stats, 0, sizeof(BatchStats), s));
@@ -485,6 +504,16 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
             }
         }
         if (need) ENS(scratch[slot], need);
+        // SW_MODE_POISON: hand-off rows a stripe reads but no earlier stripe of its item wrote come
+        // out as H = F = 496 in every s16 half (0x01f001f0): above most scores yet inside the TAG
+        // route's 511 range, so a stale read shows up as a wrong maximum instead of a wrapped
+        // (negative, ignored) tagged value
+        if ((h->mode & SW_MODE_POISON) && h->scratch[slot].p) {
+            const size_t words = h->scratch[slot].cap / 4;
+            fill_u32_kernel<<<(int)std::min<size_t>((words + 255) / 256, (size_t)h->sm_count * 8), 256, 0, s>>>(
+                reinterpret_cast<uint32_t*>(h->scratch[slot].p), words, 0x01f001f0u);
+            SW_CUDA(h, cudaGetLastError());
+        }
     }
 
     // 5. forward binning (length-sorted, longest first)
@@ -620,7 +649,7 @@ sw_status_t sw_init(sw_handle_t* handle, int device) {
         cudaMalloc(&h->d_hist, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_binbase, N_SLOTS * NBINS * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&h->d_tb, 12 * sizeof(int32_t)) != cudaSuccess ||
-        cudaMallocHost(&h->h_tb, 8 * sizeof(int32_t)) != cudaSuccess) {
+        cudaMallocHost(&h->h_tb, 12 * sizeof(int32_t)) != cudaSuccess) {
         sw_free(h);
         return SW_ERR_OUT_OF_MEMORY;
     }
@@ -816,16 +845,23 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
     bool s16_ok = false;
     sw_status_t st = check_scoring(h, scoring, sc, s16_ok);
     if (st != SW_OK) return st;
+    if (h->mode & SW_MODE_END_ONLY)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "sw_traceback needs start positions: the handle is in SW_MODE_END_ONLY");
     cudaStream_t s = (cudaStream_t)stream;
     // 1. the batch's largest interval (sizes the per-warp scratch) and the offset bases
     SW_CUDA(h, cudaMemsetAsync(h->d_tb, 0, 12 * sizeof(int32_t), s));
+    if (h->mode & SW_MODE_POISON) {
+        SW_CUDA(h, cudaMemsetAsync(n_ops, 0x7f, (size_t)n_pairs * 4, s));
+        if (h->tb_dir.p) SW_CUDA(h, cudaMemsetAsync(h->tb_dir.p, 0x7f, h->tb_dir.cap * 4, s));
+        if (h->tb_bnd.p) SW_CUDA(h, cudaMemsetAsync(h->tb_bnd.p, 0x7f, h->tb_bnd.cap * 8, s));
+    }
     int64_t* base = reinterpret_cast<int64_t*>(h->d_tb + 4);
     trace_extent_kernel<<<(int)std::min<int64_t>((n_pairs + 255) / 256, (int64_t)h->sm_count * 8), 256, 0, s>>>(
         *res, n_pairs, q_offsets, r_offsets, h->d_tb, base);
     SW_CUDA(h, cudaGetLastError());
-    SW_CUDA(h, cudaMemcpyAsync(h->h_tb, h->d_tb, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SW_CUDA(h, cudaMemcpyAsync(h->h_tb, h->d_tb, 12 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SW_CUDA(h, cudaStreamSynchronize(s));
-    const int32_t max_a = h->h_tb[0], max_b = h->h_tb[1];
+    const int32_t max_a = h->h_tb[0], max_b = h->h_tb[1], bad_intervals = h->h_tb[9];
     const int64_t q0 = reinterpret_cast<int64_t*>(h->h_tb + 4)[0], r0 = reinterpret_cast<int64_t*>(h->h_tb + 4)[1];
     // 2. one warp per pair; the warp count is capped so the direction scratch stays <= 4 GiB
     const int64_t ns = std::max<int64_t>(1, ((int64_t)max_a + TB_ROWS - 1) / TB_ROWS);
@@ -857,12 +893,17 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
     traceback_kernel<<<(int)(warps / 4), 128, 0, s>>>(T);
     SW_CUDA(h, cudaGetLastError());
     h->last_stream = s;
+    h->have_last = true;
+    h->tb_pending = true;  // the kernels' internal-error count is read by sw_batch_status
+    if (bad_intervals)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, std::to_string(bad_intervals) +
+                    " pair(s) with score > 0 have an interval outside their sequences (n_ops = -1)");
     return SW_OK;
 }
 
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
-    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32))
+    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32 | SW_MODE_POISON))
         return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
     h->mode = mode;
     return SW_OK;
@@ -972,6 +1013,12 @@ sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs) {
     SW_CUDA(h, read_stats(h, t));
     if (n_bad_pairs) *n_bad_pairs = t.n_bad;
     if (t.internal_err) return fail(h, SW_ERR_INTERNAL, "reverse-pass self-check failed");
+    if (h->tb_pending) {
+        int32_t tb_err = 0;
+        SW_CUDA(h, cudaMemcpy(&tb_err, h->d_tb + 3, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        h->tb_pending = false;
+        if (tb_err) return fail(h, SW_ERR_INTERNAL, std::to_string(tb_err) + " alignment path(s) failed (walk or scratch)");
+    }
     if (t.malformed) {
         if (n_bad_pairs) *n_bad_pairs = -1;
         return SW_ERR_BAD_PAIRS;

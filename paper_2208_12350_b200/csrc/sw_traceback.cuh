@@ -73,13 +73,15 @@ __device__ __forceinline__ int tb_pref(uint32_t c) {
     return (int)(c & 3u);
 }
 
+// The direction words were written by this warp earlier in the same kernel: every load below is
+// an L2-coherent ld.global.cg (never the non-coherent read-only path, which may return stale lines).
 template <bool RAW>
-__device__ int tb_walk(const uint32_t* __restrict__ dir, int64_t steps_pad, int a, int b, uint8_t* out) {
+__device__ int tb_walk(const uint32_t* dir, int64_t steps_pad, int a, int b, uint8_t* out) {
     int len = 0;
     int i = a, j = b, state = 0;
     int r = (a - 1) % TB_K, Lc = ((a - 1) % TB_ROWS) / TB_K;
     int64_t rowoff = (int64_t)(((a - 1) / TB_ROWS) * 32 + Lc) * steps_pad + Lc - 1;
-    uint32_t w = dir[rowoff + j];
+    uint32_t w = __ldcg(dir + rowoff + j);
     // one row up: returns true when the row's word lives in another lane's line
     auto up = [&]() -> bool {
         --i;
@@ -98,14 +100,14 @@ __device__ int tb_walk(const uint32_t* __restrict__ dir, int64_t steps_pad, int 
                 out[len++] = 'M';
                 up();
                 --j;
-                if (i > 0 && j > 0) w = dir[rowoff + j];
+                if (i > 0 && j > 0) w = __ldcg(dir + rowoff + j);
             } else {
                 state = pr;  // 1: F, 2: E
             }
         } else if (state == 1) {
             out[len++] = 'I';
             const bool open = c & 4u, ext = c & 8u;
-            if (up() && i > 0) w = dir[rowoff + j];
+            if (up() && i > 0) w = __ldcg(dir + rowoff + j);
             // H's preferred move of the cell above (row 0 is the border: E)
             const int upr = i >= 1 ? tb_pref<RAW>((w >> (5 * r)) & 31u) : 2;
             state = (open && upr == 0) ? 0 : ((ext || (open && upr == 1)) ? 1 : 0);
@@ -114,25 +116,37 @@ __device__ int tb_walk(const uint32_t* __restrict__ dir, int64_t steps_pad, int 
             const bool open = c & 16u;
             --j;
             int left = 1;  // column 0 (i >= 1): H == F
-            if (j >= 1) { w = dir[rowoff + j]; left = tb_pref<RAW>((w >> (5 * r)) & 31u); }
+            if (j >= 1) { w = __ldcg(dir + rowoff + j); left = tb_pref<RAW>((w >> (5 * r)) & 31u); }
             state = (open && left != 2) ? 0 : 2;
         }
     }
     return len > a + b ? -1 : len;
 }
 
-// Largest interval of the batch (sizes the per-warp scratch) and the offset bases.
+// A pair with S > 0 has a path only if its interval lies inside its sequences:
+// 0 <= q_start <= q_end < n and 0 <= r_start <= r_end < m.  The kernels below never trust the
+// caller's (or an earlier call's) coordinates beyond that: a pair outside it gets n_ops = -1.
+__device__ __forceinline__ bool tb_interval_ok(const sw_result_t& res, int64_t p, const int64_t* q_off, const int64_t* r_off) {
+    const int64_t n = q_off[p + 1] - q_off[p], m = r_off[p + 1] - r_off[p];
+    const int qs = res.q_start[p], qe = res.q_end[p], rs = res.r_start[p], re = res.r_end[p];
+    return qs >= 0 && qs <= qe && qe < n && rs >= 0 && rs <= re && re < m;
+}
+
+// Largest valid interval of the batch (sizes the per-warp scratch), the offset bases, and the
+// number of pairs with S > 0 whose interval is not inside their sequences (ext[9]).
 __global__ void trace_extent_kernel(sw_result_t res, int64_t n_pairs, const int64_t* q_off, const int64_t* r_off,
-                                    int32_t* ext /* [0] max a, [1] max b */, int64_t* base /* q0, r0 */) {
-    int la = 0, lb = 0;
+                                    int32_t* ext /* [0] max a, [1] max b, [9] bad intervals */, int64_t* base /* q0, r0 */) {
+    int la = 0, lb = 0, bad = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_pairs; p += (int64_t)gridDim.x * blockDim.x) {
         if (res.score[p] > 0) {
+            if (!tb_interval_ok(res, p, q_off, r_off)) { ++bad; continue; }
             la = max(la, res.q_end[p] - res.q_start[p] + 1);
             lb = max(lb, res.r_end[p] - res.r_start[p] + 1);
         }
     }
     if (la) atomicMax(ext + 0, la);
     if (lb) atomicMax(ext + 1, lb);
+    if (bad) atomicAdd(ext + 9, bad);
     if (blockIdx.x == 0 && threadIdx.x == 0) { base[0] = q_off[0]; base[1] = r_off[0]; }
 }
 
@@ -267,8 +281,8 @@ __global__ void __launch_bounds__(128) traceback_kernel(const TraceParams P) {
         const int64_t pl = pbase + lane;
         if (lane < grab && pl < P.n_pairs) {
             const int Sl = P.res.score[pl];
-            if (Sl <= 0) {
-                P.n_ops[pl] = Sl == 0 ? 0 : -1;
+            if (Sl <= 0 || !tb_interval_ok(P.res, pl, P.q_off, P.r_off)) {
+                P.n_ops[pl] = Sl == 0 ? 0 : -1;  // invalid pair, or an interval outside its sequences
             } else {
                 const int al = P.res.q_end[pl] - P.res.q_start[pl] + 1, bl = P.res.r_end[pl] - P.res.r_start[pl] + 1;
                 need = !(P.skip16 && tb16_ok(P.sc, Sl, al, bl));  // else done by traceback16_kernel
@@ -321,7 +335,7 @@ __global__ void __launch_bounds__(128) traceback16_kernel(const TraceParams P) {
             aa[h] = 0; bb[h] = 0; qs[h] = 0; rs[h] = 0;
             if (pp[h] < P.n_pairs) {
                 const int S = P.res.score[pp[h]];
-                if (S > 0) {
+                if (S > 0 && tb_interval_ok(P.res, pp[h], P.q_off, P.r_off)) {  // else the int32 kernel writes -1
                     const int a = P.res.q_end[pp[h]] - P.res.q_start[pp[h]] + 1;
                     const int b = P.res.r_end[pp[h]] - P.res.r_start[pp[h]] + 1;
                     if (tb16_ok(P.sc, S, a, b)) {

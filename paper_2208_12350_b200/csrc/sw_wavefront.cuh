@@ -252,7 +252,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                                       const int seg, const int L, const int s_m, const int (&h_pid)[T::NH],
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
                                       const int mmax, const int row0, const uint32_t o2, const uint32_t e2, const int o,
-                                      const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch) {
+                                      const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch,
+                                      const int scr_lim) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
@@ -367,7 +368,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 #pragma unroll
         for (int h = 0; h < NH; ++h)
             if (u < CD) cd[u][h] = ld_code(rp[h] + u);
-        if (MULTI) bnd[u] = (from_scratch && L == 0 && u < mmax) ? __ldcg(scr_in + u) : make_uint2(b0, 0u);
+        if (MULTI) bnd[u] = (from_scratch && L == 0 && u < scr_lim) ? __ldcg(scr_in + u) : make_uint2(b0, 0u);
     }
 
     // reverse pass: packed targets of both halves (the forward score S of each pair); the
@@ -439,9 +440,10 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             uint32_t bHO = b0, bF = 0u;
             if (MULTI) {
                 bHO = bnd[u].x; bF = bnd[u].y;
-                // columns past the item's longest reference were never handed off: they take
-                // the constant boundary, so pad-column cells stay below S (see EV above)
-                bnd[u] = (from_scratch && L == 0 && t + U < mmax) ? __ldcg(scr_in + t + U) : make_uint2(b0, 0u);
+                // only the columns the previous stripe swept were handed off (scr_lim <= mmax):
+                // past them -- the item's longest reference, or where a reverse sweep stopped
+                // early -- the constant boundary, never a stale row (see the kernel below)
+                bnd[u] = (from_scratch && L == 0 && t + U < scr_lim) ? __ldcg(scr_in + t + U) : make_uint2(b0, 0u);
             }
             // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
             const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
@@ -858,6 +860,17 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             __syncwarp();
             if (lane < SLOTS) stop[lane] = 0x7fffffff;
         }
+        // Columns of the stripe boundary row the previous stripe handed off: lane W-1 writes column
+        // c at step c + W - 1, for every step the sweep ran, so a sweep of t_sw steps hands off
+        // columns [0, min(mmax, t_sw - W + 1)).  A reverse sweep stops early (reading R6) once
+        // every half found its start or ran out of columns, and the next stripe may need columns
+        // past that point (another half of the item still searching, or the 4-column TAG block of
+        // a start that lies up to 3 columns before them); those columns must not be read from the
+        // scratch row, which still holds an earlier item's values there.  They take the constant
+        // border instead: a lower bound of the true row (H is monotone in the border values), and
+        // every such cell lies right of the columns the early stop already settled, or past the
+        // half's reversed rectangle whose cells stay < S up to the REV_PAD pad codes.
+        int scr_lim = 0;
         for (int s = 0; s < ns; ++s) {
             const int row0 = s * G::ROWS;
             // ---- build the stripe's query profile: (s - o) per (slot, code, lane, row) ----
@@ -963,21 +976,24 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             } else if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
                     steps += sweep<T, W, K, REV, false, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                     row0, o2, e2, o, nullptr, nullptr, false, false);
+                                                     row0, o2, e2, o, nullptr, nullptr, false, false, 0);
                 else
                     steps += sweep<T, W, K, REV, false, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                      row0, o2, e2, o, nullptr, nullptr, false, false);
+                                                      row0, o2, e2, o, nullptr, nullptr, false, false, 0);
             } else {
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes);
                 uint2* scr_out = reinterpret_cast<uint2*>(
                     P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
+                int t_sw;
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                    row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
+                    t_sw = sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                  row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_lim);
                 else
-                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns);
+                    t_sw = sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                   row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_lim);
+                steps += t_sw;
+                scr_lim = min(mmax, max(0, t_sw - (W - 1)));
             }
         }
         if (lane == 0) atomicAdd(P.swept, steps * G::ROWS * SLOTS);

@@ -33,6 +33,7 @@ SW_MODE_FULL = 0
 SW_MODE_END_ONLY = 1
 SW_MODE_AFFINE_ONLY = 2
 SW_MODE_TB_INT32 = 4
+SW_MODE_POISON = 8
 
 EXPORTED = ("sw_init", "sw_align_batch", "sw_align_query_db", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
@@ -207,12 +208,17 @@ def sw_dpx_peak(device: int, milliseconds: float = 200.0, stream: int = 0) -> fl
 class Aligner:
     """Owns one sw handle on one device; aligns batches held in torch tensors."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, poison: bool = False):
+        """poison=True keeps SW_MODE_POISON on (tests and soaks): every call first fills its outputs
+        and the handle's workspace with poison bytes, so an unwritten value cannot pass as a result."""
         import torch
         self.torch = torch
         self.device = int(device)
         torch.cuda.set_device(self.device)
         self.handle = sw_init(self.device)
+        self.poison = SW_MODE_POISON if poison else 0
+        if self.poison:
+            self.set_mode(SW_MODE_FULL)
 
     def close(self):
         if self.handle:
@@ -325,11 +331,19 @@ class Aligner:
 
     def traceback(self, batch) -> list:
         """Align a host batch and return each pair's op string ('' for S == 0, None for invalid)."""
+        return self.align_and_traceback(batch)[1]
+
+    def align_and_traceback(self, batch):
+        """One sw_align_batch call and the sw_traceback of ITS results: returns (the five int32
+        numpy arrays, each pair's op string ('' for S == 0, None for invalid))."""
         import torch
         q, qo, r, ro = self.to_device(batch)
         out, _ = self.align_tensors(q, qo, r, ro, batch.scoring)
         ops, n_ops = self.traceback_tensors(q, qo, r, ro, batch.scoring, out)
         torch.cuda.synchronize()
+        n = batch.n_pairs
+        o = out[:, :n].cpu().numpy()
+        fields = {k: o[i] for i, k in enumerate(("score", "q_end", "r_end", "q_start", "r_start"))}
         ops_h = ops.cpu().numpy().tobytes()
         n_h = n_ops.cpu().numpy()
         qoff, roff = batch.q_offsets, batch.r_offsets
@@ -341,12 +355,12 @@ class Aligner:
                 continue
             at = int(qoff[p] - qoff[0] + roff[p] - roff[0])
             res.append(ops_h[at:at + k].decode())
-        return res
+        return fields, res
 
     def set_mode(self, mode: int):
         """SW_MODE_FULL (forward + reverse) or SW_MODE_END_ONLY (forward only; starts not written),
         optionally OR-ed with SW_MODE_AFFINE_ONLY (linear-gap scorings stay on the affine kernels)."""
-        st = load().sw_set_mode(ctypes.c_void_p(self.handle), int(mode))
+        st = load().sw_set_mode(ctypes.c_void_p(self.handle), int(mode) | self.poison)
         if st != SW_OK:
             raise SWError(st, sw_last_error_message(self.handle))
 

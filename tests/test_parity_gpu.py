@@ -24,7 +24,9 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 def aligner():
     import torch
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
-    a = sw.Aligner(0)
+    # SW_MODE_POISON: every call first fills its outputs and the handle's workspace with poison,
+    # so a value a call did not write in that call fails the comparison instead of passing stale
+    a = sw.Aligner(0, poison=True)
     yield a
     a.close()
 
@@ -619,3 +621,63 @@ def test_traceback_s16x2_and_int32_kernels_agree(aligner, which):
     for got in (got16, got32):
         bad = [p for p in range(b.n_pairs) if got[p] != exp[p]]
         assert not bad, f"{len(bad)} paths differ; first pair {bad[0]}: gpu={got[bad[0]]!r} oracle={exp[bad[0]]!r}"
+
+
+@pytest.mark.parametrize("mismatch,gap_open", [(-1, -3), (0, -37)])
+def test_reverse_multistripe_early_stop_stale_boundary(aligner, mismatch, gap_open):
+    """Regression (round-2 root cause of the round-1 soak failure).  In a
+    multi-stripe reverse item, a half whose start lies in stripe 1 stops the item's sweep early;
+    the next stripe still sweeps up to another half's last column, and its lane 0 used to read the
+    stripe boundary row up to the item's longest reversed reference -- past the columns the
+    previous stripe had handed off, i.e. an earlier item's values.  On the TAG route a 4-column
+    block maximum above S then hid a start in the same block (q_start = r_start = -2, the reverse
+    self-check).  Half A: a 25-base exact match ending a 300 x 900 pair of C / G runs (start found
+    in stripe 1 at reversed column 24, reversed reference bound 575 columns).  Half B: q == r of
+    length L (S = L, start (0, 0) in the last reversed column, stripe >= 2); every L from 161 to
+    479 puts that column in each lane and block phase.  Poisoned workspace (hand-off rows H = F =
+    496) makes any stale read a wrong result."""
+    rng = np.random.default_rng(2022)
+    sc = {"alphabet": "dna", "match": 1, "mismatch": mismatch, "gap_open": gap_open, "gap_extend": -1}
+    alpha = list("ACGT")
+    tail = "".join(rng.choice(alpha, 25))
+    qa = "C" * 275 + tail
+    ra = "G" * 875 + tail
+    exp_a = oracle_batch(synth.from_pairs([(qa, ra)], sc))
+    assert int(exp_a["r_end"][0]) >= 600  # the long reversed reference of half A
+    for L in range(161, 480):
+        x = "".join(rng.choice(alpha, L))
+        for pairs, ia, ib in (([(qa, ra), (x, x)], 0, 1), ([(x, x), (qa, ra), (x[:L // 2 + 1], x[:L // 2 + 1])], 1, 0)):
+            b = synth.from_pairs(pairs, sc)
+            got = aligner.align(b)
+            assert tuple(int(got[f][ib]) for f in FIELDS) == (L, L - 1, L - 1, 0, 0), (L, [int(got[f][ib]) for f in FIELDS])
+            assert tuple(int(got[f][ia]) for f in FIELDS) == tuple(int(exp_a[f][0]) for f in FIELDS), L
+        st, nbad = aligner.batch_status()
+        assert st == sw.SW_OK and nbad == 0, (L, st)
+
+
+def test_soak_case_round1_whole_call(aligner):
+    """The round-1 soak pair (tests/golden/soak_case_tb16.json: fields exact, path of a 347 x 335
+    rectangle) through one sw_align_batch call whose own results feed sw_traceback, with random
+    multi-stripe partners in the same reverse work item; fields, the reverse self-check and the path
+    must all be the oracle's."""
+    import json
+    c = json.load(open(os.path.join(GOLDEN, "soak_case_tb16.json")))
+    sc, q, r = c["sc"], c["q"], c["r"]
+    exp_path = c["oracle"]
+    rng = np.random.default_rng(7)
+    for k in range(64):
+        pairs = [(q, r)]
+        for _ in range(int(rng.integers(1, 4))):
+            n = int(rng.integers(150, 520))
+            pq = "".join(rng.choice(list("ACGT"), n))
+            pr = "".join(rng.choice(list("ACGT"), int(rng.integers(300, 1300))))
+            pairs.append((pq, pr))
+        perm = rng.permutation(len(pairs))
+        pairs = [pairs[i] for i in perm]
+        at = int(np.nonzero(perm == 0)[0][0])
+        b = synth.from_pairs(pairs, sc)
+        fields, paths = aligner.align_and_traceback(b)
+        assert_parity(fields, oracle_batch(b), b)
+        assert paths[at] == exp_path, k
+        st, _ = aligner.batch_status()
+        assert st == sw.SW_OK, (k, st)

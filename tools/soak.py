@@ -32,7 +32,8 @@ def batch(rng, sc):
     alpha = "ARNDCQEGHILKMFPSTWYV" if sc["alphabet"] == "protein" else ("AC" if rng.random() < 0.3 else "ACGT")
     pairs = []
     for _ in range(int(rng.integers(1, 400))):
-        n = int(rng.integers(0, 420)) if rng.random() < 0.9 else int(rng.integers(400, 1300))
+        u = rng.random()
+        n = int(rng.integers(0, 420)) if u < 0.6 else int(rng.integers(150, 560)) if u < 0.9 else int(rng.integers(400, 1300))
         q = "".join(rng.choice(list(alpha), n))
         if rng.random() < 0.6 and n:
             mut = [c if rng.random() > 0.1 else str(rng.choice(list(alpha))) for c in q]
@@ -74,47 +75,73 @@ def soak_diffusion(rng, budget):
     return 0
 
 
+def check_fields(tag, sc, b, got, exp, nb):
+    for f in FIELDS:
+        bad = np.nonzero(got[f] != exp[f])[0]
+        if bad.size:
+            p = int(bad[0])
+            print(tag, "MISMATCH", f, sc, "batch", nb, "pair", p, b.pair(p), [int(got[k][p]) for k in FIELDS],
+                  [int(exp[k][p]) for k in FIELDS], flush=True)
+            return False
+    return True
+
+
+def save_fail(b, sc, nb, seed, p=-1):
+    import json as _json
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.savez("gpurun_out/soak_fail.npz", queries=b.queries, q_offsets=b.q_offsets, refs=b.refs,
+             r_offsets=b.r_offsets, pair=p, batch_index=nb, seed=seed)
+    _json.dump(sc, open("gpurun_out/soak_fail_scoring.json", "w"))
+
+
 def main():
+    """Every batch is drawn from one seeded generator (the seed alone replays the whole batch
+    history), aligned on a handle in SW_MODE_POISON; the five fields of EVERY call are compared
+    with the oracle -- also of the call whose results feed sw_traceback -- and sw_batch_status
+    must report no internal error after each call."""
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
     if len(sys.argv) > 2 and sys.argv[2] == "diffusion":
         return soak_diffusion(np.random.default_rng(int(time.time()) & 0xffff), budget)
     seed = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else int(time.time() * 1000) & 0xffffffff
     print(f"soak seed {seed}", flush=True)
     rng = np.random.default_rng(seed)
-    a = sw.Aligner(0)
+    a = sw.Aligner(0, poison=True)
     t0 = time.time()
-    nb = npairs = 0
+    nb = npairs = npaths = 0
     try:
         while time.time() - t0 < budget:
             sc = random_scoring(rng)
             b = batch(rng, sc)
-            got = a.align(b)
             exp = oracle.align_batch(b.queries, b.q_offsets, b.refs, b.r_offsets, b.scoring)
-            for f in FIELDS:
-                bad = np.nonzero(got[f] != exp[f])[0]
-                if bad.size:
-                    p = int(bad[0])
-                    print("MISMATCH", f, sc, p, b.pair(p), [int(got[k][p]) for k in FIELDS],
-                          [int(exp[k][p]) for k in FIELDS], flush=True)
-                    return 1
-            if rng.random() < 0.5:
-                paths = a.traceback(b)
+            with_paths = rng.random() < 0.5
+            if with_paths:
+                got, paths = a.align_and_traceback(b)
+            else:
+                got = a.align(b)
+            if not check_fields("paths" if with_paths else "fields", sc, b, got, exp, nb):
+                save_fail(b, sc, nb, seed)
+                return 1
+            st, nbad = a.batch_status()
+            if st not in (sw.SW_OK, sw.SW_ERR_BAD_PAIRS) or nbad != int(np.sum(exp["score"] < 0)):
+                print("STATUS", st, nbad, "batch", nb, sw.sw_last_error_message(a.handle), flush=True)
+                save_fail(b, sc, nb, seed)
+                return 1
+            if with_paths:
                 for p in range(b.n_pairs):
                     q, r = b.pair(p)
                     res = tuple(int(exp[k][p]) for k in FIELDS)
                     want = oracle.traceback(q, r, b.scoring, res) if res[0] >= 0 else None
                     if paths[p] != want:
-                        print("PATH MISMATCH", sc, p, (q, r), paths[p], want, flush=True)
-                        np.savez("gpurun_out/soak_fail.npz", queries=b.queries, q_offsets=b.q_offsets, refs=b.refs,
-                                 r_offsets=b.r_offsets, pair=p, batch_index=nb)
-                        import json as _json
-                        _json.dump(sc, open("gpurun_out/soak_fail_scoring.json", "w"))
+                        print("PATH MISMATCH", sc, "batch", nb, "pair", p, (q, r), paths[p], want, flush=True)
+                        save_fail(b, sc, nb, seed, p)
                         return 1
+                npaths += b.n_pairs
             nb += 1
             npairs += b.n_pairs
     finally:
         a.close()
-    print(f"soak ok: {nb} batches, {npairs} pairs, {time.time() - t0:.0f} s", flush=True)
+    print(f"soak ok: seed {seed}, {nb} batches, {npairs} pairs ({npaths} with paths), {time.time() - t0:.0f} s",
+          flush=True)
     return 0
 
 
