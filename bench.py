@@ -1,27 +1,27 @@
 #!/usr/bin/env python
 """Benchmark: batched Smith-Waterman (affine gaps) GCUPS on B200, one JSON line.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4|c2]
 
-Workload (BASELINE.json configs[1], "ADEPT-shaped DNA batch: 100k pairs, 150 bp
-reads vs contigs up to 1,024 bp, 1 B200"): the seeded synthetic batch of
-paper_2208_12350_b200.synth config "c2" (3/-3/-6/-1).  At N GPUs (torchrun, one
-rank per GPU) the global batch is c2 followed by the first (N-1)*100k pairs of
-config "c4" (the same recipe, BASELINE configs[3]), cut into N contiguous
-cell-balanced shards by sw_plan_shards: per-GPU work is fixed -> weak scaling.
+Workload (default, every N): BASELINE.json configs[3], "DNA batch of 4M pairs sharded by cell count
+across 1/2/4/8 B200" -- the seeded synthetic batch of paper_2208_12350_b200.synth config "c4"
+(4,000,000 pairs, 150 bp reads vs references of 150..1,024 bp, 3/-3/-6/-1; the ADEPT shape of
+configs[1] at 40x the size).  sw_plan_shards cuts it into N contiguous cell-balanced shards, one per
+rank: total work is fixed -> strong scaling, and the 1-GPU point is the whole 4 M batch on one GPU.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run with N ranks.
+BASELINE configs[1] (c2, 100k pairs), configs[2] (c3, protein), configs[0] (c1) and configs[4] (c5)
+are reported under `extra` at N = 1, each with its roofline fractions.
 
-A step = one sw_align_batch call (pack, binning, forward wavefront, reverse
-wavefront, finish) over the rank's shard, inputs resident in HBM; L2 (126 MB)
-is flushed between steps (a 512 MB write outside the timed events).  Time =
-sum of per-step CUDA-event times on the call's stream, max over ranks.
-`e2e` repeats the measurement through the public host-buffer API: K batches
-submitted with sw_submit_host (pinned host inputs -> H2D -> align -> D2H of the
-five result arrays, every step; step i+1's copy-in overlaps step i) then
-sw_wait, bracketed by events on the caller's stream; a single synchronous
-sw_align_batch_host call is reported beside it (latency view).
+A step = one sw_align_batch call (pack, binning, forward wavefront, reverse wavefront, finish) over
+the rank's shard, inputs resident in HBM (c4 shard >= 375 MB > the 126 MB L2 at N <= 8; L2 is also
+flushed between steps by a 512 MB write outside the timed events).  Time = sum of per-step
+CUDA-event times on the call's stream, max over ranks.  `e2e` repeats the measurement through the
+public host-buffer API: K batches submitted with sw_submit_host (pinned host inputs -> H2D -> align
+-> D2H of the five result arrays, every step; step i+1's copy-in overlaps step i) then sw_wait,
+bracketed by events on the caller's stream.
 
---impl reference runs the CPU oracle (oracle/, plain full-matrix C, all host
-cores) on a bounded sample of the same workload (rank 0 only).
+--impl reference runs the CPU oracle (oracle/, plain full-matrix C, all host cores) on a bounded
+sample of the same workload (rank 0 only).
 """
 from __future__ import annotations
 
@@ -40,7 +40,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GCUPS (DNA and protein batches) at 1/2/4/8 B200; % of DPX cell-update roofline"
-PAIRS_PER_GPU = 100_000
 FIELDS = ("score", "q_end", "r_end", "q_start", "r_start")
 
 
@@ -54,45 +53,40 @@ def parse():
                     help="skip the side measurements (other configs, modes, paths, diffusion); N > 1 runs skip them")
     ap.add_argument("--no-c5", action="store_true", help="skip the c5 (400k mixed pairs, ~1 min to generate) extra")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c4", choices=["c4", "c2"],
+                    help="the config sharded over the ranks (default c4 = BASELINE configs[3], 4 M pairs)")
     return ap.parse_args()
 
 
 # ------------------------------------------------------------------ workload
 
-def global_lengths(n_gpus: int):
-    from paper_2208_12350_b200 import synth
-    n2, m2 = synth.batch_lengths(synth.CONFIGS["c2"])
-    if n_gpus == 1:
-        return n2, m2
-    n4, m4 = synth.batch_lengths(synth.CONFIGS["c4"], 0, (n_gpus - 1) * PAIRS_PER_GPU)
-    return np.concatenate([n2, n4]), np.concatenate([m2, m4])
-
-
-def shard_range(n_gpus: int, rank: int):
-    from paper_2208_12350_b200 import sw
-    n, m = global_lengths(n_gpus)
+def shard_range(key: str, n_gpus: int, rank: int):
+    """Rank's contiguous cell-balanced pair range of config `key` (sw_plan_shards on the lengths)."""
+    from paper_2208_12350_b200 import sw, synth
+    n, m = synth.batch_lengths(synth.CONFIGS[key])
     qo = np.zeros(n.size + 1, np.int64); qo[1:] = np.cumsum(n)
     ro = np.zeros(m.size + 1, np.int64); ro[1:] = np.cumsum(m)
     cuts = sw.sw_plan_shards(qo, ro, n_gpus)
-    return int(cuts[rank]), int(cuts[rank + 1]), n.size
+    cells = n * m
+    shard_cells = [int(cells[cuts[k]:cuts[k + 1]].sum()) for k in range(n_gpus)]
+    return int(cuts[rank]), int(cuts[rank + 1]), n.size, shard_cells
 
 
-def make_shard(lo: int, hi: int):
-    """Pairs [lo, hi) of the global batch (c2 then c4)."""
+def make_shard(key: str, lo: int, hi: int, world: int):
+    """Pairs [lo, hi) of config `key` (generated on this rank's share of the host cores)."""
     from paper_2208_12350_b200 import synth
-    parts = []
-    c2n = synth.CONFIGS["c2"].n_pairs
-    if lo < c2n:
-        parts.append(synth.generate("c2", lo, min(hi, c2n)))
-    if hi > c2n:
-        parts.append(synth.generate("c4", max(lo, c2n) - c2n, hi - c2n))
-    if len(parts) == 1:
-        return parts[0]
-    a, b = parts
-    qo = np.concatenate([a.q_offsets, b.q_offsets[1:] + a.q_offsets[-1]])
-    ro = np.concatenate([a.r_offsets, b.r_offsets[1:] + a.r_offsets[-1]])
-    return synth.Batch(np.concatenate([a.queries, b.queries]), qo, np.concatenate([a.refs, b.refs]), ro,
-                       a.scoring, "c2+c4")
+    workers = max(1, min(32, (os.cpu_count() or 1) // max(world, 1)))
+    return synth.generate_parallel(key, lo, hi, workers=workers)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 # ------------------------------------------------------------------ clocks
@@ -289,6 +283,28 @@ def simcov_extra(torch, no_cpu: bool) -> dict:
     return res
 
 
+def config_extra(a, sw, synth, torch, key, flush_buf, peak_gcups, steps=3, warmup=2):
+    """One BASELINE config at 1 GPU, whole batch in one call: whole-call and forward-kernel GCUPS and
+    their fractions of the measured DPX roofline (SURVEY 8.0.1 #9: frac = GCUPS / roofline)."""
+    bx = synth.generate_parallel(key)
+    qx, qox, rx, rox = a.to_device(bx)
+    ox = a.alloc_out(bx.n_pairs)
+    tx, sx = time_device_steps(a, qx, qox, rx, rox, bx.scoring, ox, steps, warmup, flush_buf, torch)
+    med = float(np.median(tx))
+    fwd = float(np.median([x["fwd"] for x in sx]))
+    rev = float(np.median([x["rev"] for x in sx]))
+    del qx, qox, rx, rox, ox
+    cells = bx.cells()
+    call = cells / med / 1e6
+    fk = cells / fwd / 1e6
+    return {"workload": synth.CONFIGS[key].name, "pairs": bx.n_pairs, "cells": cells,
+            "gcups": round(call, 1), "ms": round(med, 3), "fwd_kernel_gcups": round(fk, 1),
+            "frac_call": round(call / peak_gcups, 4), "frac_fwd": round(fk / peak_gcups, 4),
+            "rev_share_of_call": round(rev / med, 4),
+            "stage_ms": {k: round(float(np.median([x[k] for x in sx])), 4) for k in sx[0]},
+            "batch_sha256": synth.batch_sha256(bx)}
+
+
 def run_ours(args, rank: int, world: int, local_rank: int):
     import torch
     import torch.distributed as dist
@@ -296,8 +312,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device(f"cuda:{local_rank}")
-    lo, hi, n_global = shard_range(world, rank)
-    batch = make_shard(lo, hi)
+    key = args.workload
+    lo, hi, n_global, shard_cells = shard_range(key, world, rank)
+    batch = make_shard(key, lo, hi, world)
+    sha = synth.batch_sha256(batch)
     cells = batch.cells()
     a = sw.Aligner(local_rank)
     a.enable_stage_timing(True)
@@ -307,6 +325,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # roofline denominator: measured DPX Gotoh-mix rate on this GPU, same process
     peak_cups = sw.sw_dpx_peak(local_rank, 300.0, torch.cuda.current_stream().cuda_stream)
+    peak_gcups = peak_cups / 1e9
 
     if world > 1:
         dist.barrier()
@@ -321,6 +340,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         if time.perf_counter() > t_end + 5.0:
             break
     clocks.lines.clear()
+    if world > 1:
+        dist.barrier()
     times, stages = time_device_steps(a, q, qo, r, ro, batch.scoring, out, args.steps, args.warmup, flush_buf, torch)
     torch.cuda.synchronize()
     if world > 1:
@@ -333,9 +354,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ---- e2e through the public host-buffer API (pinned host buffers) ----
     # K steps as a stream of batches (sw_submit_host / sw_wait): every step copies its inputs
-    # from pinned host memory (75 MB for c2), aligns, and copies the five result arrays back;
-    # step i+1's copy-in overlaps step i's alignment.  Events on the caller's stream bracket
-    # the whole stream (the first copy-in waits for e0, sw_wait joins the last copy-out).
+    # from pinned host memory, aligns, and copies the five result arrays back; step i+1's
+    # copy-in overlaps step i's alignment.  Events on the caller's stream bracket the whole
+    # stream (the first copy-in waits for e0, sw_wait joins the last copy-out).
     qh = torch.from_numpy(np.ascontiguousarray(batch.queries)).pin_memory()
     rh = torch.from_numpy(np.ascontiguousarray(batch.refs)).pin_memory()
     qoh = torch.from_numpy(np.ascontiguousarray(batch.q_offsets)).pin_memory()
@@ -357,6 +378,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     check(sw.sw_wait(a.handle))
     flush_buf.zero_()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for k in range(args.steps):
@@ -367,87 +390,75 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e_total = float(e0.elapsed_time(e1))
     # results of the host path must equal the device path
     same = bool(torch.equal(outh[(args.steps - 1) & 1], out[:, :batch.n_pairs].cpu()))
-    # one synchronous call (sw_align_batch_host: chunked, two streams) for the latency view
-    sync_ms = []
-    for k in range(3):
-        flush_buf.zero_()
-        torch.cuda.synchronize()
-        f0 = torch.cuda.Event(enable_timing=True); f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(s)
-        check(sw.sw_align_batch_host(a.handle, qh.data_ptr(), qoh.data_ptr(), rh.data_ptr(), roh.data_ptr(),
-                                     batch.n_pairs, batch.scoring, ptrs[0], s.cuda_stream))
-        f1.record(s)
-        f1.synchronize()
-        sync_ms.append(f0.elapsed_time(f1))
-    sync_ms = float(np.median(sync_ms))
     clk = clocks.stop()  # sampled over the device-timed and the e2e-timed regions
 
     # ---- aggregate over ranks: max time ----
     vals = torch.tensor([total_ms, e2e_total, stage_med["fwd"]], dtype=torch.float64, device=dev)
-    cells_t = torch.tensor([cells, fwd_cells], dtype=torch.float64, device=dev)
+    cells_t = torch.tensor([cells, fwd_cells, own * args.steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
         dist.all_reduce(cells_t, op=dist.ReduceOp.SUM)
     total_ms, e2e_total, fwd_ms_max = [float(x) for x in vals.tolist()]
     all_cells = float(cells_t[0].item())
+    all_launches = int(cells_t[2].item())
 
     extra = {}
     if rank == 0 and world == 1 and not args.no_extra:
-        for key in ("c3", "c1") + (() if args.no_c5 else ("c5",)):
-            bx = synth.generate(key)
-            qx, qox, rx, rox = a.to_device(bx)
-            ox = a.alloc_out(bx.n_pairs)
-            tx, sx = time_device_steps(a, qx, qox, rx, rox, bx.scoring, ox, 3, 1 if key == "c5" else 2, flush_buf, torch)
-            med = float(np.median(tx))
-            del qx, qox, rx, rox
-            extra[key] = {"workload": synth.CONFIGS[key].name + (" (the 8-GPU config at 1 GPU)" if key == "c5" else ""),
-                          "gcups": round(bx.cells() / med / 1e6, 1),
-                          "ms": round(med, 3), "fwd_kernel_gcups": round(bx.cells() / float(np.median([x["fwd"] for x in sx])) / 1e6, 1),
-                          "stage_ms": {k: round(float(np.median([x[k] for x in sx])), 4) for k in sx[0]}}
+        keys = ("c2", "c3", "c1") + (() if args.no_c5 else ("c5",))
+        for kx in keys:
+            if kx == key:
+                continue
+            extra[kx] = config_extra(a, sw, synth, torch, kx, flush_buf, peak_gcups,
+                                     warmup=1 if kx == "c5" else 2)
+        if "c5" in extra:
+            extra["c5"]["workload"] += " (the 8-GPU config at 1 GPU)"
 
     if rank == 0 and world == 1 and not args.no_extra:
-        # forward pass only (SW_MODE_END_ONLY: score, q_end, r_end), the same shard
+        # side measurements on the ADEPT-shaped c2 batch (BASELINE configs[1])
+        b2 = batch if key == "c2" else synth.generate_parallel("c2")
+        c2cells = b2.cells()
+        q2, qo2, r2, ro2 = a.to_device(b2)
+        out2 = a.alloc_out(b2.n_pairs)
+        # forward pass only (SW_MODE_END_ONLY: score, q_end, r_end)
         a.set_mode(sw.SW_MODE_END_ONLY)
-        te, se = time_device_steps(a, q, qo, r, ro, batch.scoring, out, 5, 2, flush_buf, torch)
+        te, se = time_device_steps(a, q2, qo2, r2, ro2, b2.scoring, out2, 5, 2, flush_buf, torch)
         a.set_mode(sw.SW_MODE_FULL)
         med = float(np.median(te))
-        extra["end_only"] = {"workload": "rank-0 shard, SW_MODE_END_ONLY (forward pass only)", "ms": round(med, 3),
-                             "gcups": round(cells / med / 1e6, 1)}
-        # alignment paths of the same shard (sw_traceback) after the full alignment
-        a.align_tensors(q, qo, r, ro, batch.scoring, out=out)
-        ops, n_ops = a.traceback_tensors(q, qo, r, ro, batch.scoring, out)
+        extra["end_only"] = {"workload": "c2, SW_MODE_END_ONLY (forward pass only)", "ms": round(med, 3),
+                             "gcups": round(c2cells / med / 1e6, 1)}
+        # alignment paths (sw_traceback) after the full alignment
+        a.align_tensors(q2, qo2, r2, ro2, b2.scoring, out=out2)
+        ops, n_ops = a.traceback_tensors(q2, qo2, r2, ro2, b2.scoring, out2)
         torch.cuda.synchronize()
         tt = []
         for _ in range(5):
             g0 = torch.cuda.Event(enable_timing=True); g1 = torch.cuda.Event(enable_timing=True)
             g0.record()
-            a.traceback_tensors(q, qo, r, ro, batch.scoring, out, ops, n_ops)
+            a.traceback_tensors(q2, qo2, r2, ro2, b2.scoring, out2, ops, n_ops)
             g1.record()
             g1.synchronize()
             tt.append(g0.elapsed_time(g1))
-        o5 = out[:, :batch.n_pairs].cpu().numpy().astype(np.int64)
+        o5 = out2[:, :b2.n_pairs].cpu().numpy().astype(np.int64)
         icells = int(np.sum(np.where(o5[0] > 0, (o5[1] - o5[3] + 1) * (o5[2] - o5[4] + 1), 0)))
         med = float(np.median(tt))
-        extra["traceback"] = {"workload": "rank-0 shard, sw_traceback after sw_align_batch", "ms": round(med, 3),
+        extra["traceback"] = {"workload": "c2, sw_traceback after sw_align_batch", "ms": round(med, 3),
                               "interval_cells": icells, "interval_gcups": round(icells / med / 1e6, 1),
-                              "pairs_per_s": round(batch.n_pairs / med * 1e3, 1),
-                              "ops_total": int(n_ops[:batch.n_pairs].clamp(min=0).sum().item())}
-
-    if rank == 0 and world == 1 and not args.no_extra:
-        # linear gaps (gap_open == gap_extend: the two-state kernels), same shard
+                              "pairs_per_s": round(b2.n_pairs / med * 1e3, 1),
+                              "ops_total": int(n_ops[:b2.n_pairs].clamp(min=0).sum().item())}
+        del ops, n_ops
+        # linear gaps (gap_open == gap_extend: the two-state kernels)
         lin = {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -4, "gap_extend": -4}
-        out_x = a.alloc_out(batch.n_pairs)  # keep `out` (the headline run's results) for the parity leg
-        tl, sl = time_device_steps(a, q, qo, r, ro, lin, out_x, 5, 2, flush_buf, torch)
+        tl, sl = time_device_steps(a, q2, qo2, r2, ro2, lin, out2, 5, 2, flush_buf, torch)
         med = float(np.median(tl))
-        extra["linear_gap"] = {"workload": "rank-0 shard, DNA 3/-3, gap -4 per residue (two-state kernels)",
-                               "ms": round(med, 3), "gcups": round(cells / med / 1e6, 1),
-                               "fwd_kernel_gcups": round(cells / float(np.median([x["fwd"] for x in sl])) / 1e6, 1)}
-        # one query against the shard's references (sw_align_query_db)
-        n0 = int(batch.q_offsets[1] - batch.q_offsets[0])
-        qd = q[:max(n0, 1)].clone()
-        qcells = float(n0) * float(batch.r_offsets[-1] - batch.r_offsets[0])
-        res = sw.sw_result_t(*[out_x[i].data_ptr() for i in range(5)])
-        sc_db = sw.make_scoring(batch.scoring)
+        extra["linear_gap"] = {"workload": "c2, DNA 3/-3, gap -4 per residue (two-state kernels)",
+                               "ms": round(med, 3), "gcups": round(c2cells / med / 1e6, 1),
+                               "fwd_kernel_gcups": round(c2cells / float(np.median([x["fwd"] for x in sl])) / 1e6, 1)}
+        # one query against c2's references (sw_align_query_db)
+        n0 = int(b2.q_offsets[1] - b2.q_offsets[0])
+        qd = q2[:max(n0, 1)].clone()
+        qcells = float(n0) * float(b2.r_offsets[-1] - b2.r_offsets[0])
+        res = sw.sw_result_t(*[out2[i].data_ptr() for i in range(5)])
+        sc_db = sw.make_scoring(b2.scoring)
         lib_ = sw.load()
         tq = []
         for k in range(7):
@@ -456,7 +467,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             flush_buf.zero_()
             e0.record()
             stq = lib_.sw_align_query_db(ctypes.c_void_p(a.handle), ctypes.c_void_p(qd.data_ptr()), n0,
-                                         ctypes.c_void_p(r.data_ptr()), ctypes.c_void_p(ro.data_ptr()), batch.n_pairs,
+                                         ctypes.c_void_p(r2.data_ptr()), ctypes.c_void_p(ro2.data_ptr()), b2.n_pairs,
                                          ctypes.byref(sc_db), ctypes.byref(res),
                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
             e1.record()
@@ -466,8 +477,9 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             if k >= 2:
                 tq.append(e0.elapsed_time(e1))
         med = float(np.median(tq))
-        extra["query_db"] = {"workload": f"one {n0}-bp query vs the shard's {batch.n_pairs} references",
+        extra["query_db"] = {"workload": f"one {n0}-bp query vs c2's {b2.n_pairs} references",
                              "ms": round(med, 3), "gcups": round(qcells / med / 1e6, 1)}
+        del q2, qo2, r2, ro2, out2
         extra["simcov"] = simcov_extra(torch, args.no_cpu_baseline)
 
     cpu = None
@@ -475,6 +487,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sub, o, dt, cores = oracle_sample(batch)
         cpu = {"value": round(sub.cells() / dt / 1e9, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": f"first {sub.n_pairs} pairs of the rank-0 shard ({sub.cells():.3e} forward cells), "
                          f"forward+reverse, {dt:.1f} s"}
         gpu = out[:, :sub.n_pairs].cpu().numpy()
@@ -486,7 +499,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         return
     value = all_cells * args.steps / (total_ms * 1e-3) / 1e9
     fwd_gcups = cells / (stage_med["fwd"] * 1e-3) / 1e9  # rank-0 dominant kernel, live events
-    peak_gcups = peak_cups / 1e9
+    call_gcups = cells / (float(np.median(times)) * 1e-3) / 1e9  # rank-0 whole sw_align_batch call
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_fwd_traffic.json")
     if os.path.exists(prof):
@@ -495,6 +508,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         except (OSError, ValueError):
             traffic = None
     h2d = int(batch.queries.nbytes + batch.refs.nbytes + batch.q_offsets.nbytes + batch.r_offsets.nbytes)
+    cfg = synth.CONFIGS[key]
     line = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -504,29 +518,30 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         "warmup": args.warmup,
         "ms_per_step": round(total_ms / args.steps, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "int16",
         "data": "synthetic",
-        "config": {"workload": "c2_dna_100k_150x1024 (BASELINE configs[1])" if world == 1 else
-                   f"c2 + c4[:{(world - 1) * PAIRS_PER_GPU}] = {n_global} pairs, cell-balanced shards",
-                   "pairs": n_global, "pairs_per_gpu": batch.n_pairs, "cells_per_gpu": cells,
+        "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.index - 1}]: {cfg.baseline_text})",
+                   "pairs": n_global, "pairs_rank0": batch.n_pairs, "cells_total": int(sum(shard_cells)),
+                   "cells_per_rank": shard_cells, "shard_imbalance": round(max(shard_cells) / (sum(shard_cells) / world), 5),
                    "scoring": "DNA 3/-3/-6/-1", "step": "sw_align_batch: pack+bin+fwd+rev+finish",
-                   "l2": "flushed between steps (512 MB write outside timed events)",
-                   "parallelism": f"dp{world}"},
+                   "sharding": "sw_plan_shards: contiguous cell-balanced ranges, no collective",
+                   "l2": "rank shard > 126 MB L2; also flushed between steps (512 MB write outside timed events)",
+                   "batch_sha256_rank0": sha, "parallelism": f"dp{world}"},
         "roofline": {"bound": "alu", "achieved": round(fwd_gcups, 1), "peak": round(peak_gcups, 1), "unit": "GCUPS",
                      "frac": round(fwd_gcups / peak_gcups, 4), "traffic": traffic,
-                     "kernel": "wavefront_kernel<TS16,16,10,fwd>",
+                     "kernel": "wavefront_kernel<TS16,16,10,fwd,TAG> (forward pass, rank 0)",
+                     "frac_call": round(call_gcups / peak_gcups, 4),
+                     "frac_call_note": "whole sw_align_batch call GCUPS (rank 0) / peak: SURVEY 8.0.1 #9",
                      "peak_source": "sw_dpx_peak: measured s16x2 Gotoh 5.5-instr cell-pair mix, this GPU, this run",
                      "peak_derived_gcups": round(148 * 2 * 32 * 1.965e9 * 2 / 5.5 / 1e9, 1)},
         "e2e": {"value": round(all_cells * args.steps / (e2e_total * 1e-3) / 1e9, 1), "unit": "GCUPS",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 5 * 4 * batch.n_pairs,
+                "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": 5 * 4 * n_global,
                 "api": "sw_submit_host x steps + sw_wait (pinned host buffers; copy-in of step i+1 overlaps step i)",
                 "ms_per_step": round(e2e_total / args.steps, 4),
-                "single_call_ms": round(sync_ms, 4),
-                "single_call_gcups": round(cells / (sync_ms * 1e-3) / 1e9, 1),
                 "matches_device_path": same},
-        "gpu_launches": int(own * args.steps),
+        "gpu_launches": all_launches,
         "library_sort_calls": int(lib * args.steps),
         "clocks": clk,
         "stage_ms": {k: round(v, 4) for k, v in stage_med.items()},
@@ -548,8 +563,22 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(args) -> int:
+    """`--gpus N` (N > 1) without torchrun: re-run this script under torch.distributed.run with N
+    ranks on this node (127.0.0.1 rendezvous); rank 0's JSON line is the output."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -151,18 +151,41 @@ sw_status_t sw_init(sw_handle_t* handle, int device);
  *   out               HOST struct of DEVICE pointers (see sw_result_t)
  *   stream            a cudaStream_t (NULL = legacy default stream)
  * Work is enqueued on `stream`; inputs and outputs must stay untouched until
- * it completes.  The call synchronises on `stream` once (to read the
- * per-batch length statistics that size the launches; the first call of a
- * handle, or one whose payload outgrows the handle's code buffers, also reads
- * the payload extents q/r_offsets[0], [n_pairs] first), so it returns after
- * earlier work on `stream` is done but before this batch's kernels finish.  Per-pair errors do not fail the
- * call: they appear as -1 sentinels and are counted by sw_batch_status.
+ * it completes.  Asynchrony:
+ *   - after sw_reserve, a batch within the reservation is enqueued without any
+ *     host round trip: the call returns at once and can be captured into a
+ *     CUDA graph.  A batch beyond the reservation (payload, pair count, or a
+ *     sequence longer than the reserved lengths) and malformed offsets are
+ *     detected on the device: every output is -1 and sw_batch_status returns
+ *     SW_ERR_INVALID_ARGUMENT / SW_ERR_BAD_PAIRS (count -1).
+ *   - without a reservation, the call synchronises on `stream` once (to read
+ *     the per-batch length statistics that size the launches; the first call
+ *     of a handle, or one whose payload outgrows the handle's code buffers,
+ *     also reads the payload extents first), so it returns after earlier work
+ *     on `stream` is done but before this batch's kernels finish; malformed
+ *     offsets return SW_ERR_INVALID_ARGUMENT (every output -1).
+ * Per-pair errors do not fail the call: they appear as -1 sentinels and are
+ * counted by sw_batch_status.
  */
 sw_status_t sw_align_batch(sw_handle_t h,
                            const uint8_t* queries, const int64_t* q_offsets,
                            const uint8_t* refs, const int64_t* r_offsets,
                            int64_t n_pairs, const sw_scoring_t* scoring,
                            const sw_result_t* out, void* stream);
+
+/*
+ * Reserve the handle's workspace for batches of up to max_pairs pairs,
+ * max_query_bytes / max_ref_bytes payload bytes (q_offsets[n]-q_offsets[0],
+ * r_offsets[n]-r_offsets[0]) and sequences of up to max_query_len /
+ * max_ref_len residues (<= SW_MAX_SEQ_LEN).  Afterwards sw_align_batch (and
+ * sw_align_query_db once its broadcast buffer exists) never synchronises for a
+ * batch with n_pairs <= max_pairs: launches are sized from the reservation
+ * and the device-side counts.  Synchronises the device; may be called again
+ * (the workspace only grows).  Errors: SW_ERR_INVALID_ARGUMENT (bounds out of
+ * range), SW_ERR_OUT_OF_MEMORY, SW_ERR_WRONG_DEVICE.
+ */
+sw_status_t sw_reserve(sw_handle_t h, int64_t max_pairs, int64_t max_query_bytes, int64_t max_ref_bytes,
+                       int32_t max_query_len, int32_t max_ref_len);
 
 /*
  * One query against a database of references (the
@@ -221,7 +244,10 @@ sw_status_t sw_submit_host(sw_handle_t h,
 sw_status_t sw_wait(sw_handle_t h);
 
 /* Synchronise the handle's last batch and report how many pairs were
- * invalid.  Returns SW_OK, SW_ERR_BAD_PAIRS (count > 0) or SW_ERR_INTERNAL. */
+ * invalid.  Returns SW_OK, SW_ERR_BAD_PAIRS (count > 0; -1 for malformed
+ * offsets), SW_ERR_INVALID_ARGUMENT (a reserved call's batch beyond the
+ * reservation) or SW_ERR_INTERNAL (a device self-check, incl. sw_traceback's
+ * path walks since the previous sw_batch_status). */
 sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs);
 
 /* Synchronise outstanding work, release the workspace and the handle. */

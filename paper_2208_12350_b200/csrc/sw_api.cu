@@ -57,6 +57,13 @@ const void* wave_kernel_ptr(bool protein, int route) {
                : (const void*)wavefront_kernel<TS16, W16, K16, REV, false, LIN>;
 }
 
+void wave_kernels(bool protein, bool lin, const void** kfwd, const void** krev) {
+    for (int r = 0; r < N_ROUTES; ++r) {
+        kfwd[r] = lin ? wave_kernel_ptr<false, true>(protein, r) : wave_kernel_ptr<false, false>(protein, r);
+        krev[r] = lin ? wave_kernel_ptr<true, true>(protein, r) : wave_kernel_ptr<true, false>(protein, r);
+    }
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
@@ -122,6 +129,11 @@ struct sw_context {
     cudaStream_t as_stream = nullptr;    // the caller's stream of the submitted batches
 
     int codes_alphabet = -1;  // alphabet the code buffers were last cleared for
+    // sw_reserve: bounds the workspace was sized for; device-buffer calls within them never
+    // synchronise (enqueue and return, capturable in a CUDA graph)
+    bool reserved = false;
+    int64_t res_pairs = 0, res_qbytes = 0, res_rbytes = 0;
+    int32_t res_n = 0, res_m = 0;
     cudaStream_t copy_stream = nullptr;  // host-buffer entry point: overlapped copies
     cudaEvent_t ev_in[MAX_CHUNKS] = {}, ev_out[MAX_CHUNKS] = {}, ev_prep = nullptr;
     bool timing = false;
@@ -243,6 +255,46 @@ Launch plan_wave(const sw_context* h, const void* kernel, int nc, int64_t n_path
     return l;
 }
 
+// Grids of the forward / reverse wavefront launches of every route (persistent, at most one
+// resident wave; the kernels pull work items up to the device-side counts).
+void plan_waves(const sw_context* h, const Scoring& sc, bool protein, const BatchStats& hs, const void* const* kfwd,
+                const void* const* krev, Launch* lf, Launch* lr) {
+    for (int r = 0; r < N_ROUTES; ++r) {
+        // reverse-pass pairs are a subset of the forward ones (finish_fwd may move TAG pairs to
+        // S16): forward counts bound the grids
+        const bool demote = (int64_t)sc.max_sigma * hs.max_n > TAG_MAX_SCORE;  // finish_fwd's TAG -> S16 rule
+        const int64_t rev_upper = hs.fwd_count[r] + (r == ROUTE_S16 && demote ? hs.fwd_count[ROUTE_TAG] : 0);
+        if (r == ROUTE_S32) {
+            lf[r] = plan_wave<G32>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
+            lr[r] = plan_wave<G32>(h, krev[r], sc.nc, rev_upper);
+        } else if (protein) {
+            // 3-warp blocks: 5 blocks x 3 warps fit the SM's shared memory (4-warp blocks: only 3)
+            lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], 3);
+            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, rev_upper, 3);
+        } else {
+            lf[r] = plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
+            lr[r] = plan_wave<G16>(h, krev[r], sc.nc, rev_upper);
+        }
+    }
+}
+
+// Stripe hand-off scratch of a call: per resident warp, segment and parity, one boundary row
+// (HO, F) of the longest reference (+ fill/drain); zero unless some query spans two stripes.
+size_t scratch_bytes(const Launch* lf, const Launch* lr, const BatchStats& hs, bool protein, int64_t& seg_bytes) {
+    size_t need = 0;
+    seg_bytes = 0;
+    const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16) * 8;
+    for (int r = 0; r < N_ROUTES; ++r) {
+        const int rows = r == ROUTE_S32 ? G32::ROWS : protein ? GP::ROWS : G16::ROWS;
+        const int segs = r == ROUTE_S32 ? G32::SEGS : protein ? GP::SEGS : G16::SEGS;
+        if (hs.fwd_count[r] && hs.max_n > rows) {
+            seg_bytes = row_bytes;
+            need = std::max(need, (size_t)std::max(lf[r].blocks * lf[r].warps, lr[r].blocks * lr[r].warps) * segs * 2 * row_bytes);
+        }
+    }
+    return need;
+}
+
 // What the host already knows about a batch (host-buffer entry point): with it the
 // pipeline needs no stream synchronisation between enqueueing and completion.
 struct HostPlan {
@@ -284,7 +336,7 @@ cudaError_t read_stats(sw_context* h, BatchStats& t) {
     for (int k = 1; k < N_SLOTS; ++k) {
         const BatchStats& u = h->h_stats[k];
         t.n_bad += u.n_bad; t.internal_err += u.internal_err; t.cells += u.cells;
-        t.swept_fwd += u.swept_fwd; t.swept_rev += u.swept_rev; t.malformed |= u.malformed;
+        t.swept_fwd += u.swept_fwd; t.swept_rev += u.swept_rev; t.malformed |= u.malformed; t.rejected |= u.rejected;
     }
     return cudaSuccess;
 }
@@ -299,7 +351,7 @@ sw_status_t bin_order(sw_context* h, int32_t* order, int64_t lo, int64_t hi, boo
     if (small) {
         bin_scan_kernel<<<1, BIN_SCAN_THREADS, BIN_SCAN_SMEM, s>>>(hist, base);
         const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)h->sm_count * 8);
-        bin_scatter_kernel<<<blocks, 256, 0, s>>>(h->key.p, base, order, lo, hi);
+        bin_scatter_kernel<<<blocks, 256, 0, s>>>(h->key.p, base, order, lo, hi, &h->d_stats[slot].malformed);
         SW_CUDA(h, cudaGetLastError());
         h->own_launches += 2;
         return SW_OK;
@@ -352,13 +404,16 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         return fail(h, SW_ERR_INVALID_ARGUMENT, "NULL pointer argument");
     h->last_stream = s;
     h->have_last = true;
+    // reserved call (sw_reserve): nothing is read back; launches are sized from the reservation and
+    // the device-side counts, and pack rejects a batch beyond the reservation on the device
+    const bool async = !hp && !host_ext && h->reserved && n_pairs <= h->res_pairs;
 
     // 1. payload extents
     int64_t ext[4] = {0, 0, 0, 0};
     // speculative extents (device-buffer calls once the code buffers exist): pack reads the
     // extents itself and checks they fit the buffers' capacity; the host learns the outcome from
     // the statistics read-back it does anyway (one host round trip per call instead of two)
-    const bool spec = !hp && !host_ext && !h->no_spec_ext && h->qcode.cap > 0 && h->rcode.cap > 0 && h->rrev.cap > 0;
+    const bool spec = async || (!hp && !host_ext && !h->no_spec_ext && h->qcode.cap > 0 && h->rcode.cap > 0 && h->rrev.cap > 0);
     if (hp) {
         std::memcpy(ext, hp->ext, sizeof(ext));
     } else if (host_ext) {
@@ -418,6 +473,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         P.rows_s16 = rows16; P.rows_s32 = rows32;
         P.ext_dev = spec ? 1 : 0; P.n_all = n_pairs;
         P.qcap = (int64_t)h->qcode.cap; P.rcap = (int64_t)std::min(h->rcode.cap, h->rrev.cap);
+        P.cap_n = async ? h->res_n : 0; P.cap_m = async ? h->res_m : 0;
         P.qcode = h->qcode.p; P.rcode = h->rcode.p;
         P.nlen = h->nlen.p; P.mlen = h->mlen.p; P.qpos = h->qpos.p; P.rpos = h->rpos.p; P.flags = h->flags.p; P.key = h->key.p;
         P.hist = hist; P.keys_fwd = h->keys_fwd.p; P.iota = h->iota.p; P.stats = stats;
@@ -431,7 +487,10 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
     // forward binning enqueued before the read-back below, assuming the common small-region
     // batch: the GPU bins while the host waits; a batch outside it is re-sorted (radix) after
-    const bool spec_bin = !hp;
+    // (a reserved call knows from the reservation whether every key lies in the small region)
+    const int min_rows0 = std::min(rows16, G32::ROWS);
+    const bool res_small = async && h->res_m < BIN_COLS && (h->res_n + min_rows0 - 1) / min_rows0 <= BIN_MAX_STRIPES;
+    const bool spec_bin = !hp && (!async || res_small);
     if (spec_bin) {
         st = bin_order(h, h->order.p + lo, lo, hi, true, slot, s);
         if (st != SW_OK) return st;
@@ -444,6 +503,13 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         hs.max_n = hp->max_n;
         hs.max_m = hp->max_m;
         for (int r = 0; r < N_ROUTES; ++r) hs.fwd_count[r] = hp->route_upper[r];
+    } else if (async) {
+        // bounds from the reservation: every route may hold every pair (the persistent grids read
+        // the real counts on the device), lengths up to the reserved ones
+        std::memset(&hs, 0, sizeof(hs));
+        hs.max_n = h->res_n;
+        hs.max_m = h->res_m;
+        for (int r = 0; r < N_ROUTES; ++r) hs.fwd_count[r] = (int32_t)n_pairs;
     } else {
         SW_CUDA(h, cudaMemcpyAsync(h->h_stats, stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
         SW_CUDA(h, cudaStreamSynchronize(s));
@@ -467,42 +533,14 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     const bool lin = sc.gap_open == sc.gap_extend && !(h->mode & SW_MODE_AFFINE_ONLY);
     const void* kfwd[N_ROUTES];
     const void* krev[N_ROUTES];
-    for (int r = 0; r < N_ROUTES; ++r) {
-        kfwd[r] = lin ? wave_kernel_ptr<false, true>(protein, r) : wave_kernel_ptr<false, false>(protein, r);
-        krev[r] = lin ? wave_kernel_ptr<true, true>(protein, r) : wave_kernel_ptr<true, false>(protein, r);
-    }
+    wave_kernels(protein, lin, kfwd, krev);
     Launch lf[N_ROUTES], lr[N_ROUTES];
-    for (int r = 0; r < N_ROUTES; ++r) {
-        // reverse-pass pairs are a subset of the forward ones (finish_fwd may move TAG pairs to
-        // S16): forward counts bound the grids
-        const bool demote = (int64_t)sc.max_sigma * hs.max_n > TAG_MAX_SCORE;  // finish_fwd's TAG -> S16 rule
-        const int64_t rev_upper = hs.fwd_count[r] + (r == ROUTE_S16 && demote ? hs.fwd_count[ROUTE_TAG] : 0);
-        if (r == ROUTE_S32) {
-            lf[r] = plan_wave<G32>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
-            lr[r] = plan_wave<G32>(h, krev[r], sc.nc, rev_upper);
-        } else if (protein) {
-            // 3-warp blocks: 5 blocks x 3 warps fit the SM's shared memory (4-warp blocks: only 3)
-            lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], 3);
-            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, rev_upper, 3);
-        } else {
-            lf[r] = plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
-            lr[r] = plan_wave<G16>(h, krev[r], sc.nc, rev_upper);
-        }
-    }
+    plan_waves(h, sc, protein, hs, kfwd, krev, lf, lr);
 
     // stripe hand-off scratch: only if some query spans more than one stripe
     int64_t seg_bytes = 0;
     {
-        size_t need = 0;
-        const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16) * 8;
-        for (int r = 0; r < N_ROUTES; ++r) {
-            const int rows = r == ROUTE_S32 ? rows32 : rows16;
-            const int segs = r == ROUTE_S32 ? G32::SEGS : protein ? GP::SEGS : G16::SEGS;
-            if (hs.fwd_count[r] && hs.max_n > rows) {
-                seg_bytes = row_bytes;
-                need = std::max(need, (size_t)std::max(lf[r].blocks * lf[r].warps, lr[r].blocks * lr[r].warps) * segs * 2 * row_bytes);
-            }
-        }
+        const size_t need = scratch_bytes(lf, lr, hs, protein, seg_bytes);
         if (need) ENS(scratch[slot], need);
         // SW_MODE_POISON: hand-off rows a stripe reads but no earlier stripe of its item wrote come
         // out as H = F = 496 in every s16 half (0x01f001f0): above most scores yet inside the TAG
@@ -535,6 +573,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     W.one = 1;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p + lo;
     W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &stats->swept_fwd; W.counts = stats->fwd_count;
+    W.stats = stats;
     for (int r = 0; r < N_ROUTES; ++r) {
         if (lf[r].blocks <= 0) continue;
         W.route = r;
@@ -680,6 +719,61 @@ sw_status_t sw_align_batch(sw_handle_t h, const uint8_t* queries, const int64_t*
                            const sw_result_t* out, void* stream) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
     return align_impl(h, queries, q_offsets, refs, r_offsets, n_pairs, scoring, out, (cudaStream_t)stream, nullptr);
+}
+
+sw_status_t sw_reserve(sw_handle_t h, int64_t max_pairs, int64_t max_query_bytes, int64_t max_ref_bytes,
+                       int32_t max_query_len, int32_t max_ref_len) {
+    if (!h) return SW_ERR_INVALID_ARGUMENT;
+    if (max_pairs < 1 || max_pairs > 0x7ffffff0LL || max_query_bytes < 0 || max_ref_bytes < 0 || max_query_len < 0 ||
+        max_ref_len < 0 || max_query_len > SW_MAX_SEQ_LEN || max_ref_len > SW_MAX_SEQ_LEN)
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "sw_reserve: bounds out of range");
+    int dev = -1;
+    SW_CUDA(h, cudaGetDevice(&dev));
+    if (dev != h->device) return fail(h, SW_ERR_WRONG_DEVICE, "current device differs from the handle's device");
+    SW_CUDA(h, cudaDeviceSynchronize());  // buffers may move: nothing of the handle may be in flight
+    h->reserved = false;
+    const size_t N = (size_t)max_pairs;
+    sw_status_t st = prepare_workspace(h, N, (size_t)max_query_bytes, (size_t)max_ref_bytes, h->codes_alphabet < 0 ? 0 : h->codes_alphabet, 0);
+    if (st != SW_OK) return st;
+    // radix-sort temporary storage (reserved calls whose keys may leave the counting sort's region)
+    {
+        size_t tb = 0;
+        SW_CUDA(h, cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, h->key.p, h->key_sorted.p, h->iota.p,
+                                                             h->order.p, (int)max_pairs, 0, 32, (cudaStream_t)0));
+        st = ensure(h, h->cub_temp[0], tb);
+        if (st != SW_OK) return st;
+    }
+    // stripe hand-off scratch for the largest grid of any alphabet / gap model / route
+    BatchStats hs;
+    std::memset(&hs, 0, sizeof(hs));
+    hs.max_n = max_query_len;
+    hs.max_m = max_ref_len;
+    for (int r = 0; r < N_ROUTES; ++r) hs.fwd_count[r] = (int32_t)max_pairs;
+    size_t need = 0;
+    for (int pr = 0; pr < 2; ++pr)
+        for (int lin = 0; lin < 2; ++lin) {
+            Scoring sc;
+            std::memset(&sc, 0, sizeof(sc));
+            sc.alphabet = pr ? SW_ALPHABET_PROTEIN : SW_ALPHABET_DNA;
+            sc.nc = pr ? NC_PROTEIN : NC_DNA;
+            sc.max_sigma = 32767;
+            const void* kf[N_ROUTES];
+            const void* kr[N_ROUTES];
+            wave_kernels(pr != 0, lin != 0, kf, kr);
+            Launch lf[N_ROUTES], lr[N_ROUTES];
+            plan_waves(h, sc, pr != 0, hs, kf, kr, lf, lr);
+            int64_t seg = 0;
+            need = std::max(need, scratch_bytes(lf, lr, hs, pr != 0, seg));
+        }
+    if (need) {
+        st = ensure(h, h->scratch[0], need);
+        if (st != SW_OK) return st;
+    }
+    SW_CUDA(h, cudaDeviceSynchronize());
+    h->res_pairs = max_pairs; h->res_qbytes = max_query_bytes; h->res_rbytes = max_ref_bytes;
+    h->res_n = max_query_len; h->res_m = max_ref_len;
+    h->reserved = true;
+    return SW_OK;
 }
 
 namespace {
@@ -1013,6 +1107,10 @@ sw_status_t sw_batch_status(sw_handle_t h, int64_t* n_bad_pairs) {
     SW_CUDA(h, read_stats(h, t));
     if (n_bad_pairs) *n_bad_pairs = t.n_bad;
     if (t.internal_err) return fail(h, SW_ERR_INTERNAL, "reverse-pass self-check failed");
+    if (t.rejected) {
+        if (n_bad_pairs) *n_bad_pairs = -1;
+        return fail(h, SW_ERR_INVALID_ARGUMENT, "the batch exceeds the handle's reservation (sw_reserve): every output is -1");
+    }
     if (h->tb_pending) {
         int32_t tb_err = 0;
         SW_CUDA(h, cudaMemcpy(&tb_err, h->d_tb + 3, sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -1036,6 +1134,7 @@ sw_status_t sw_free(sw_handle_t h) {
     for (int k = 0; k < N_SLOTS; ++k) { release(h->cub_temp[k]); release(h->scratch[k]); } release(h->keys_fwd); release(h->keys_rev);
     release(h->qcode); release(h->rcode); release(h->rrev);
     release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
+    release(h->db_q); release(h->db_qo);
     if (h->d_stats) cudaFree(h->d_stats);
     if (h->h_stats) cudaFreeHost(h->h_stats);
     if (h->h_ext) cudaFreeHost(h->h_ext);

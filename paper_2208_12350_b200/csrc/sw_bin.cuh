@@ -89,11 +89,14 @@ __global__ void __launch_bounds__(BIN_SCAN_THREADS) bin_scan_kernel(uint32_t* hi
     for (int k = t; k < NBINS; k += BIN_SCAN_THREADS) base[k] = s_h[bin_pad(k)];
 }
 
-// order[base[bin(key[p])]++] = p for every pair with work (small-region batches only).
+// order[base[bin(key[p])]++] = p for every pair with work (small-region batches only).  `reject`
+// (optional) points at BatchStats::malformed, overflow, rejected: a rejected batch scatters nothing.
 // Warp-aggregated: lanes holding the same bin (reverse keys cluster on a few scores) take
 // their slots with one atomic per distinct bin of the warp.
 __global__ void __launch_bounds__(256) bin_scatter_kernel(const uint32_t* key, uint32_t* base, int32_t* order, int64_t lo,
-                                                         int64_t hi) {
+                                                         int64_t hi, const int32_t* reject) {
+    if (reject && (((const volatile int32_t*)reject)[0] | ((const volatile int32_t*)reject)[1] |
+                   ((const volatile int32_t*)reject)[2])) return;  // batch_rejected (sw_pack.cuh)
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t p0 = lo + (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); p0 < hi; p0 += stride) {

@@ -55,6 +55,13 @@ constexpr int FIN_FB = SW_FIN_FB;   // words per lane loaded before any is store
 
 __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     __shared__ int s_route[N_ROUTES];
+    if (batch_rejected(P.stats)) {  // whole batch invalid (malformed / beyond the reservation): every field -1
+        for (int64_t p = P.lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.hi; p += (int64_t)gridDim.x * blockDim.x) {
+            P.out.score[p] = -1; P.out.q_end[p] = -1; P.out.r_end[p] = -1;
+            if (!P.end_only) { P.out.q_start[p] = -1; P.out.r_start[p] = -1; }
+        }
+        return;
+    }
     if (threadIdx.x < N_ROUTES) s_route[threadIdx.x] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -181,6 +188,7 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
 // After the reverse pass: q_start = q_end - i', r_start = r_end - j'.
 // Self-check (pin P14 on the device): the reverse maximum must equal S.
 __global__ void __launch_bounds__(256) finish_rev_kernel(FinishParams P) {
+    if (batch_rejected(P.stats)) return;  // finish_fwd wrote -1 everywhere
     int err = 0;
     for (int64_t p = P.lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.hi; p += (int64_t)gridDim.x * blockDim.x) {
         if (P.flags[p] & FLAG_BAD) continue;

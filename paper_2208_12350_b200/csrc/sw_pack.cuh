@@ -21,10 +21,23 @@ struct BatchStats {
     int32_t max_m;          // longest valid reference
     int32_t malformed;      // offsets decrease somewhere -> whole batch invalid
     int32_t overflow;       // speculative extents: the payload did not fit the code buffers (nothing packed)
+    int32_t rejected;       // reserved (asynchronous) call: the batch exceeds the reservation (sw_reserve)
     int32_t fwd_count[4];   // valid, non-trivial pairs per route (forward pass)
     int32_t rev_count[4];   // pairs with S > 0 per route (reverse pass)
 };
 constexpr size_t STATS_PER_BATCH_OFFSET = offsetof(BatchStats, max_n);
+
+// Whole-batch failure flags set by pack (malformed offsets, speculative extents that did not fit,
+// a reserved call's batch beyond its reservation): every later kernel of the call checks them at
+// entry and does nothing (finish_fwd then writes -1 to every output), so a call enqueued without a
+// host round trip never reads per-pair state pack did not write.
+static_assert(offsetof(BatchStats, overflow) == offsetof(BatchStats, malformed) + 4 &&
+              offsetof(BatchStats, rejected) == offsetof(BatchStats, malformed) + 8,
+              "bin_scatter_kernel reads the three flags from &malformed");
+__device__ __forceinline__ bool batch_rejected(const BatchStats* st) {
+    const volatile BatchStats* v = st;
+    return (v->malformed | v->overflow | v->rejected) != 0;
+}
 
 struct PackParams {
     const uint8_t* queries;
@@ -37,6 +50,7 @@ struct PackParams {
     int ext_dev;                 // read the extents from q_off / r_off here (no host round trip) and check
     int64_t n_all;               //   they fit qcap / rcap (else stats->overflow, nothing written)
     int64_t qcap, rcap;
+    int32_t cap_n, cap_m;        // reserved call (sw_reserve): longest query / reference it covers (0: none)
     int alphabet;
     int s16_ok;                  // scoring fits the s16x2 path (int8 profile, int16 range)
     int tag_ok;                  // the ROUTE_TAG kernel geometry supports row tags
@@ -174,7 +188,7 @@ constexpr int PACK_FB = SW_PACK_FB;      // 16-byte vectors per lane in flight
 // byte-wise (only this warp's bytes).
 __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
     constexpr int PPW = PACK_PPW;
-    __shared__ int s_bad, s_route[N_ROUTES], s_maxn, s_maxm, s_malformed;
+    __shared__ int s_bad, s_route[N_ROUTES], s_maxn, s_maxm, s_malformed, s_reject;
     __shared__ unsigned long long s_cells;
     __shared__ uint8_t lut[256];
     __shared__ int64_t s_slot[PACK_WARPS][PPW];   // rcode slot start rp - PADL
@@ -183,7 +197,7 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
     __shared__ int64_t s_qa[PACK_WARPS][PPW];     // query payload starts
     __shared__ uint32_t s_badbits[PACK_WARPS];
     if (threadIdx.x == 0) {
-        s_bad = s_maxn = s_maxm = s_malformed = 0;
+        s_bad = s_maxn = s_maxm = s_malformed = s_reject = 0;
         for (int r = 0; r < N_ROUTES; ++r) s_route[r] = 0;
         s_cells = 0;
     }
@@ -205,14 +219,17 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
             return;
         }
         if ((qN - q0) + 32 > P.qcap || (rN - r0) + P.n_all * (PADL + PADR) + GUARD + 16 > P.rcap) {
-            if (blockIdx.x == 0 && threadIdx.x == 0) P.stats->overflow = 1;
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                if (P.cap_n) P.stats->rejected = 1;  // reserved call: beyond the reservation
+                else P.stats->overflow = 1;
+            }
             return;  // uniform over the grid: nothing is written, the host grows and re-runs
         }
     }
     const uint8_t pad_code = (uint8_t)((P.alphabet == SW_ALPHABET_DNA ? NC_DNA : NC_PROTEIN) - 1);
     const uint32_t padw = (uint32_t)pad_code * 0x01010101u;
     const bool dna = P.alphabet == SW_ALPHABET_DNA;
-    int l_bad = 0, l_route[N_ROUTES] = {0, 0, 0}, l_maxn = 0, l_maxm = 0, l_malf = 0;
+    int l_bad = 0, l_route[N_ROUTES] = {0, 0, 0}, l_maxn = 0, l_maxm = 0, l_malf = 0, l_rej = 0;
     unsigned long long l_cells = 0;
     int64_t* slot = s_slot[wib];
     int64_t* rdelta = s_rdelta[wib];
@@ -365,6 +382,7 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
                 }
                 l_maxn = max(l_maxn, nn);
                 l_maxm = max(l_maxm, mm);
+                if (P.cap_n && (nn > P.cap_n || mm > P.cap_m)) l_rej = 1;
             }
             P.nlen[p] = nn;
             P.mlen[p] = mm;
@@ -384,6 +402,7 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
     if (l_maxn) atomicMax(&s_maxn, l_maxn);
     if (l_maxm) atomicMax(&s_maxm, l_maxm);
     if (l_malf) atomicOr(&s_malformed, 1);
+    if (l_rej) atomicOr(&s_reject, 1);
     if (l_cells) atomicAdd(&s_cells, l_cells);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -393,6 +412,7 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
         if (s_maxn) atomicMax(&P.stats->max_n, s_maxn);
         if (s_maxm) atomicMax(&P.stats->max_m, s_maxm);
         if (s_malformed) atomicOr(&P.stats->malformed, 1);
+        if (s_reject) atomicOr(&P.stats->rejected, 1);
         if (s_cells) atomicAdd(&P.stats->cells, s_cells);
     }
 }

@@ -115,6 +115,7 @@ struct WaveParams {
     uint32_t tag_mul;           // = 64; a kernel parameter so the row tag is an IMAD (FMA pipe), not a LEA
     uint32_t one;               // = 1; a kernel parameter so H = Hb + o is an IMAD (FMA pipe), not an IADD3
     Scoring sc;
+    const BatchStats* stats;    // whole-batch failure flags (batch_rejected)
 };
 
 template <int W, int K, class T>
@@ -762,6 +763,7 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
     // cell of the query's rows whatever the columns hold (end events, reverse pass alike).
     constexpr bool TAGF = TAG;
     extern __shared__ __align__(16) uint8_t smem[];
+    if (batch_rejected(P.stats)) return;  // nothing of this call was packed (uniform over the grid)
     // substitution table for the profile builds, in shared memory: lanes index it with
     // divergent codes, which a constant-bank table would serialise
     __shared__ int8_t s_sigma[24 * 24];

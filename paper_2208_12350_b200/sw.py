@@ -35,7 +35,7 @@ SW_MODE_AFFINE_ONLY = 2
 SW_MODE_TB_INT32 = 4
 SW_MODE_POISON = 8
 
-EXPORTED = ("sw_init", "sw_align_batch", "sw_align_query_db", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
+EXPORTED = ("sw_init", "sw_reserve", "sw_align_batch", "sw_align_query_db", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",
             "sw_get_stage_ms", "sw_last_launch_count", "sw_last_cell_counts", "sw_last_reverse_cells", "sw_dpx_peak")
 
@@ -80,6 +80,7 @@ def load(build_if_missing: bool = True):
     rp = ctypes.POINTER(sw_result_t)
     lib.sw_init.argtypes = [ctypes.POINTER(vp), ctypes.c_int]
     lib.sw_align_batch.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
+    lib.sw_reserve.argtypes = [vp, i64, i64, i64, i32, i32]
     lib.sw_align_batch_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
     lib.sw_align_query_db.argtypes = [vp, vp, i64, vp, vp, i64, sp, rp, vp]
     lib.sw_submit_host.argtypes = [vp, vp, vp, vp, vp, i64, sp, rp, vp]
@@ -219,6 +220,20 @@ class Aligner:
         self.poison = SW_MODE_POISON if poison else 0
         if self.poison:
             self.set_mode(SW_MODE_FULL)
+
+    def reserve(self, max_pairs: int, max_query_bytes: int, max_ref_bytes: int, max_query_len: int, max_ref_len: int):
+        """sw_reserve: afterwards calls within these bounds enqueue without a host round trip."""
+        st = load().sw_reserve(ctypes.c_void_p(self.handle), int(max_pairs), int(max_query_bytes), int(max_ref_bytes),
+                               int(max_query_len), int(max_ref_len))
+        if st != SW_OK:
+            raise SWError(st, sw_last_error_message(self.handle))
+
+    def reserve_for(self, batch, pairs_slack: float = 1.0):
+        """Reservation sized for `batch` (times `pairs_slack` on counts and bytes)."""
+        n, m = batch.lengths()
+        k = max(pairs_slack, 1.0)
+        self.reserve(int(batch.n_pairs * k) + 1, int(n.sum() * k) + 1, int(m.sum() * k) + 1,
+                     int(n.max()) if n.size else 0, int(m.max()) if m.size else 0)
 
     def close(self):
         if self.handle:

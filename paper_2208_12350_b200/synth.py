@@ -228,6 +228,50 @@ def generate(cfg: Config | str, start: int = 0, stop: int | None = None) -> Batc
     return Batch(qa.astype(np.uint8), qo, ra.astype(np.uint8), ro, dict(cfg.scoring), f"{cfg.name}[{start}:{stop}]")
 
 
+def _gen_range(args):
+    key, start, stop = args
+    b = generate(key, start, stop)
+    return b.queries, np.diff(b.q_offsets), b.refs, np.diff(b.r_offsets)
+
+
+def generate_parallel(cfg: Config | str, start: int = 0, stop: int | None = None, workers: int | None = None) -> Batch:
+    """generate() split over worker processes by whole blocks: byte-identical to generate(cfg, start,
+    stop) (every block draws from its own seed), for the large configs (c4: 4 M pairs)."""
+    import multiprocessing as mp
+    import os
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    stop = cfg.n_pairs if stop is None else min(stop, cfg.n_pairs)
+    workers = workers or min(32, os.cpu_count() or 1)
+    if workers <= 1 or stop - start <= 4 * BLOCK:
+        return generate(cfg, start, stop)
+    key = next(k for k, v in CONFIGS.items() if v is cfg)
+    step = max(BLOCK, ((stop - start) // (4 * workers) + BLOCK - 1) // BLOCK * BLOCK)
+    cuts = list(range(start, stop, step)) + [stop]
+    jobs = [(key, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    with mp.get_context("fork").Pool(workers) as pool:
+        parts = pool.map(_gen_range, jobs)
+    n = np.concatenate([p[1] for p in parts])
+    m = np.concatenate([p[3] for p in parts])
+    qo = np.zeros(n.size + 1, np.int64)
+    ro = np.zeros(m.size + 1, np.int64)
+    qo[1:] = np.cumsum(n)
+    ro[1:] = np.cumsum(m)
+    return Batch(np.concatenate([p[0] for p in parts]), qo, np.concatenate([p[2] for p in parts]), ro,
+                 dict(cfg.scoring), f"{cfg.name}[{start}:{stop}]")
+
+
+def batch_sha256(b: Batch) -> str:
+    """SHA-256 over the batch's CSR arrays and scoring (the reproducibility record of SURVEY 8(d))."""
+    import hashlib
+    import json
+    h = hashlib.sha256()
+    for arr in (b.q_offsets, b.queries, b.r_offsets, b.refs):
+        h.update(np.ascontiguousarray(arr).tobytes())
+    h.update(json.dumps(b.scoring, sort_keys=True).encode())
+    return h.hexdigest()
+
+
 def random_pairs(seed: int, count: int, n_range, m_range, alphabet: bytes = b"ACGT", scoring=None,
                  name="random") -> Batch:
     """Unrelated i.i.d. pairs over ``alphabet`` (tests: tiny/adversarial sets)."""

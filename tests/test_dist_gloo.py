@@ -77,24 +77,22 @@ def test_reductions_without_process_group():
     np.testing.assert_array_equal(out["score"], np.arange(4))
 
 
-def test_bench_weak_scaling_shards():
-    """bench.py's N-GPU workload: c2 + c4 prefix, contiguous cell-balanced shards."""
+def test_bench_strong_scaling_shards():
+    """bench.py's workload at N GPUs: BASELINE configs[3] (c4, 4 M pairs) cut into N contiguous
+    cell-balanced shards by sw_plan_shards (strong scaling: the 1-GPU point is the whole batch)."""
     import bench
     from paper_2208_12350_b200 import synth as s
-    n, m = bench.global_lengths(4)
-    assert n.size == 4 * bench.PAIRS_PER_GPU
-    prev = 0
-    cells = []
-    for rank in range(4):
-        lo, hi, total = bench.shard_range(4, rank)
-        assert lo == prev and total == n.size
-        cells.append(int(np.sum(n[lo:hi] * m[lo:hi])))
-        prev = hi
-    assert prev == n.size
-    assert max(cells) / (sum(cells) / 4) < 1.001
-    # a shard straddling the c2 / c4 boundary is the concatenation of both generators
-    c2n = s.CONFIGS["c2"].n_pairs
-    b = bench.make_shard(c2n - 3, c2n + 2)
-    want = [s.generate("c2", c2n - 3, c2n).pair(k) for k in range(3)] + \
-           [s.generate("c4", 0, 2).pair(k) for k in range(2)]
-    assert [b.pair(k) for k in range(5)] == want
+    n, m = s.batch_lengths(s.CONFIGS["c4"])
+    assert n.size == 4_000_000
+    for world in (1, 2, 4, 8):
+        prev = 0
+        for rank in range(world):
+            lo, hi, total, shard_cells = bench.shard_range("c4", world, rank)
+            assert lo == prev and total == n.size and len(shard_cells) == world
+            assert shard_cells[rank] == int(np.sum(n[lo:hi] * m[lo:hi]))
+            prev = hi
+        assert prev == n.size
+        assert max(shard_cells) / (sum(shard_cells) / world) < 1.0001
+    # a rank's shard is byte-identical to the serial generator's pairs
+    b = bench.make_shard("c4", 123_456, 123_456 + 3000, 2)
+    assert s.batch_sha256(b) == s.batch_sha256(s.generate("c4", 123_456, 123_456 + 3000))

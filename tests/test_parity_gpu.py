@@ -681,3 +681,129 @@ def test_soak_case_round1_whole_call(aligner):
         assert paths[at] == exp_path, k
         st, _ = aligner.batch_status()
         assert st == sw.SW_OK, (k, st)
+
+
+# ------------------------------------------------- reserved (asynchronous) calls
+
+def _reserved_aligner(b, slack=1.0):
+    a = sw.Aligner(0, poison=True)
+    a.reserve_for(b, slack)
+    return a
+
+
+@pytest.mark.parametrize("which", ["c1", "c2_prefix", "c3_prefix", "c5_mixed"])
+def test_reserved_call_matches_oracle(which):
+    """After sw_reserve, sw_align_batch enqueues without a host round trip (launches sized from the
+    reservation, device-side counts); results are the oracle's on every config shape, including
+    multi-stripe queries and long references (radix-sort path of the reservation)."""
+    if which == "c1":
+        b = synth.generate("c1")
+    elif which == "c2_prefix":
+        b = synth.generate("c2", 0, 3000)
+    elif which == "c3_prefix":
+        b = synth.generate("c3", 0, 800)
+    else:
+        full = synth.generate("c5", 0, 2048)
+        n, m = full.lengths()
+        idx = [int(p) for p in np.argsort(n * m)[:1900]]  # the bounded-oracle-cost part, incl. long pairs
+        b = full.subset(sorted(idx))
+    a = _reserved_aligner(b, 1.5)
+    try:
+        for _ in range(2):
+            assert_parity(a.align(b), oracle_batch(b), b)
+            assert a.batch_status() == (sw.SW_OK, 0)
+        # a smaller batch within the same reservation
+        sub = b.subset(range(0, b.n_pairs, 3))
+        assert_parity(a.align(sub), oracle_batch(sub), sub)
+    finally:
+        a.close()
+
+
+def test_reserved_call_returns_before_the_gpu_finishes():
+    """Enqueue-and-return: with a reservation the call does not wait for earlier work on its stream
+    (a 0.3 s device sleep is still running when it returns); without one it does."""
+    import time
+    import torch
+    b = synth.generate("c2", 0, 2000)
+    a = sw.Aligner(0)
+    try:
+        q, qo, r, ro = a.to_device(b)
+        out = a.alloc_out(b.n_pairs)
+        a.align_tensors(q, qo, r, ro, b.scoring, out=out)
+        torch.cuda.synchronize()
+        cycles = int(0.3 * 1.9e9)
+
+        def timed_call():
+            torch.cuda._sleep(cycles)
+            t0 = time.perf_counter()
+            a.align_tensors(q, qo, r, ro, b.scoring, out=out)
+            dt = time.perf_counter() - t0
+            torch.cuda.synchronize()
+            return dt
+
+        t_sync = timed_call()
+        a.reserve_for(b)
+        t_async = timed_call()
+        assert t_sync > 0.1, t_sync
+        assert t_async < 0.05, t_async
+        got = out[:, :b.n_pairs].cpu().numpy()
+        assert_parity({f: got[i] for i, f in enumerate(FIELDS)}, oracle_batch(b), b)
+    finally:
+        a.close()
+
+
+def test_reserved_call_captured_in_cuda_graph():
+    """A reserved call contains no synchronisation or allocation, so it can be captured into a CUDA
+    graph; every replay rewrites the outputs with the oracle's results."""
+    import torch
+    b = synth.generate("c2", 0, 1500)
+    a = sw.Aligner(0)
+    try:
+        a.reserve_for(b)
+        q, qo, r, ro = a.to_device(b)
+        out = a.alloc_out(b.n_pairs)
+        a.align_tensors(q, qo, r, ro, b.scoring, out=out)  # warm (module load, attributes)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        with torch.cuda.graph(g, stream=cs):
+            a.align_tensors(q, qo, r, ro, b.scoring, out=out)
+        exp = oracle_batch(b)
+        for _ in range(3):
+            out.fill_(-7)
+            g.replay()
+            torch.cuda.synchronize()
+            got = out[:, :b.n_pairs].cpu().numpy()
+            assert_parity({f: got[i] for i, f in enumerate(FIELDS)}, exp, b)
+    finally:
+        a.close()
+
+
+def test_reserved_call_rejects_batches_beyond_the_reservation():
+    """Beyond the reservation (longer sequences, more payload) or with malformed offsets, a reserved
+    call is rejected on the device: every output -1, reported by sw_batch_status; the handle keeps
+    working for batches within the reservation."""
+    import torch
+    small = synth.generate("c1", 0, 200)
+    a = sw.Aligner(0, poison=True)
+    try:
+        a.reserve_for(small)
+        longer = synth.from_pairs([("ACGT" * 100, "ACGT" * 100)] + [small.pair(k) for k in range(5)], small.scoring)
+        got = a.align(longer, check=False)
+        assert all(np.all(got[f] == -1) for f in FIELDS)
+        st, nbad = a.batch_status()
+        assert st == sw.SW_ERR_INVALID_ARGUMENT and nbad == -1
+        assert_parity(a.align(small), oracle_batch(small), small)
+        assert a.batch_status() == (sw.SW_OK, 0)
+        q, qo, r, ro = a.to_device(small)
+        qo_bad = qo.clone()
+        qo_bad[7] = qo_bad[9] + 5  # decreasing offsets inside the batch
+        out = a.alloc_out(small.n_pairs)
+        a.align_tensors(q, qo_bad, r, ro, small.scoring, out=out, check=False)
+        torch.cuda.synchronize()
+        assert bool((out[:, :small.n_pairs] == -1).all())
+        st, nbad = a.batch_status()
+        assert st == sw.SW_ERR_BAD_PAIRS and nbad == -1
+        assert_parity(a.align(small), oracle_batch(small), small)
+    finally:
+        a.close()

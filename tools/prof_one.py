@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 import torch
 from paper_2208_12350_b200 import sw, synth
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-b = synth.generate(cfg)
+b = synth.generate_parallel(cfg)
 a = sw.Aligner(0)
 q, qo, r, ro = a.to_device(b)
 out = a.alloc_out(b.n_pairs)

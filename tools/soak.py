@@ -1,5 +1,8 @@
 """Randomised parity soak (development tool): random batches under random valid scorings, every
-field and every alignment path compared with the oracle.  python tools/soak.py [seconds]"""
+field and every alignment path compared with the oracle.
+    python tools/soak.py [seconds] [seed]              fields + paths vs the oracle
+    python tools/soak.py [seconds] invariance [seed]   batch invariance at GPU speed (+ oracle sample)
+    python tools/soak.py [seconds] diffusion           the diffusion stencil vs oracle/diffusion.py"""
 from __future__ import annotations
 
 import os
@@ -94,6 +97,78 @@ def save_fail(b, sc, nb, seed, p=-1):
     _json.dump(sc, open("gpurun_out/soak_fail_scoring.json", "w"))
 
 
+def fast_batch(rng, sc, count):
+    """A larger random batch built with numpy (invariance soak): mixed lengths including multi-stripe
+    queries and long references, half of the pairs related (the query embedded with substitutions)."""
+    alpha = np.frombuffer(b"ARNDCQEGHILKMFPSTWYV" if sc["alphabet"] == "protein" else b"ACGT", dtype=np.uint8)
+    if sc["alphabet"] == "dna" and rng.random() < 0.3:
+        alpha = alpha[:2]
+    u = rng.random(count)
+    n = np.where(u < 0.5, rng.integers(0, 300, count), np.where(u < 0.9, rng.integers(150, 700, count),
+                                                                  rng.integers(600, 2500, count)))
+    pairs = []
+    for k in range(count):
+        q = alpha[rng.integers(0, alpha.size, int(n[k]))]
+        if rng.random() < 0.5 and n[k]:
+            r = q.copy()
+            mut = rng.random(r.size) < rng.choice([0.02, 0.1, 0.3])
+            r[mut] = alpha[rng.integers(0, alpha.size, int(mut.sum()))]
+            r = np.concatenate([alpha[rng.integers(0, alpha.size, int(rng.integers(0, 200)))], r,
+                                alpha[rng.integers(0, alpha.size, int(rng.integers(0, 200)))]])
+        else:
+            r = alpha[rng.integers(0, alpha.size, int(rng.integers(0, 1500)))]
+        pairs.append((q.tobytes(), r.tobytes()))
+    return synth.from_pairs(pairs, sc)
+
+
+def soak_invariance(seed, budget):
+    """Batch invariance (pin P11) at GPU speed: each random batch is aligned whole, permuted and
+    split into random sub-batches, on a poisoned handle; every pair's five fields must agree bit for
+    bit across the calls, and a random sample is checked against the oracle."""
+    rng = np.random.default_rng(seed)
+    a = sw.Aligner(0, poison=True)
+    t0 = time.time()
+    nb = npairs = 0
+    try:
+        while time.time() - t0 < budget:
+            sc = random_scoring(rng)
+            b = fast_batch(rng, sc, int(rng.integers(500, 6000)))
+            ref = a.align(b)
+            perm = rng.permutation(b.n_pairs)
+            got = a.align(b.subset(perm))
+            inv = {f: np.empty_like(ref[f]) for f in FIELDS}
+            for f in FIELDS:
+                inv[f][perm] = got[f]
+            if not check_fields("permuted", sc, b, inv, ref, nb):
+                save_fail(b, sc, nb, seed)
+                return 1
+            cuts = np.sort(rng.choice(np.arange(1, b.n_pairs), size=min(3, b.n_pairs - 1), replace=False))
+            parts = np.split(np.arange(b.n_pairs), cuts)
+            for part in parts:
+                sub = b.subset(part)
+                g = a.align(sub)
+                if not check_fields("split", sc, sub, g, {f: ref[f][part] for f in FIELDS}, nb):
+                    save_fail(b, sc, nb, seed)
+                    return 1
+            idx = np.sort(rng.choice(b.n_pairs, size=min(48, b.n_pairs), replace=False))
+            sub = b.subset(idx)
+            exp = oracle.align_batch(sub.queries, sub.q_offsets, sub.refs, sub.r_offsets, sub.scoring)
+            if not check_fields("oracle-sample", sc, sub, {f: ref[f][idx] for f in FIELDS}, exp, nb):
+                save_fail(b, sc, nb, seed)
+                return 1
+            st, _ = a.batch_status()
+            if st not in (sw.SW_OK, sw.SW_ERR_BAD_PAIRS):
+                print("STATUS", st, "batch", nb, flush=True)
+                return 1
+            nb += 1
+            npairs += b.n_pairs
+    finally:
+        a.close()
+    print(f"invariance soak ok: seed {seed}, {nb} batches, {npairs} pairs x {2 + 1} calls, {time.time() - t0:.0f} s",
+          flush=True)
+    return 0
+
+
 def main():
     """Every batch is drawn from one seeded generator (the seed alone replays the whole batch
     history), aligned on a handle in SW_MODE_POISON; the five fields of EVERY call are compared
@@ -102,6 +177,10 @@ def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
     if len(sys.argv) > 2 and sys.argv[2] == "diffusion":
         return soak_diffusion(np.random.default_rng(int(time.time()) & 0xffff), budget)
+    if len(sys.argv) > 2 and sys.argv[2] == "invariance":
+        seed = int(sys.argv[3]) if len(sys.argv) > 3 else int(time.time() * 1000) & 0xffffffff
+        print(f"invariance soak seed {seed}", flush=True)
+        return soak_invariance(seed, budget)
     seed = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else int(time.time() * 1000) & 0xffffffff
     print(f"soak seed {seed}", flush=True)
     rng = np.random.default_rng(seed)
