@@ -283,7 +283,8 @@ void plan_waves(const sw_context* h, const Scoring& sc, bool protein, const Batc
 size_t scratch_bytes(const Launch* lf, const Launch* lr, const BatchStats& hs, bool protein, int64_t& seg_bytes) {
     size_t need = 0;
     seg_bytes = 0;
-    const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16) * 8;
+    // W slack slots before column 0, the item's longest reference plus fill / drain / prefetch after it
+    const int64_t row_bytes = ((int64_t)hs.max_m + 64 + 16 + 16) * 8;
     for (int r = 0; r < N_ROUTES; ++r) {
         const int rows = r == ROUTE_S32 ? G32::ROWS : protein ? GP::ROWS : G16::ROWS;
         const int segs = r == ROUTE_S32 ? G32::SEGS : protein ? GP::SEGS : G16::SEGS;
@@ -541,7 +542,11 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     int64_t seg_bytes = 0;
     {
         const size_t need = scratch_bytes(lf, lr, hs, protein, seg_bytes);
-        if (need) ENS(scratch[slot], need);
+        if (need && h->scratch[slot].cap < need) {
+            ENS(scratch[slot], need);
+            // defined contents: the first stripe of an item loads (and discards) its row
+            SW_CUDA(h, cudaMemsetAsync(h->scratch[slot].p, 0, h->scratch[slot].cap, s));
+        }
         // SW_MODE_POISON: hand-off rows a stripe reads but no earlier stripe of its item wrote come
         // out as H = F = 496 in every s16 half (0x01f001f0): above most scores yet inside the TAG
         // route's 511 range, so a stale read shows up as a wrong maximum instead of a wrapped
@@ -768,6 +773,7 @@ sw_status_t sw_reserve(sw_handle_t h, int64_t max_pairs, int64_t max_query_bytes
     if (need) {
         st = ensure(h, h->scratch[0], need);
         if (st != SW_OK) return st;
+        SW_CUDA(h, cudaMemset(h->scratch[0].p, 0, h->scratch[0].cap));
     }
     SW_CUDA(h, cudaDeviceSynchronize());
     h->res_pairs = max_pairs; h->res_qbytes = max_query_bytes; h->res_rbytes = max_ref_bytes;

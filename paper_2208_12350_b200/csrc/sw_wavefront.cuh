@@ -33,7 +33,7 @@
 //   sign-extends them into an s16x2 operand;
 // * queries longer than W*K rows are processed as stripes; lane W-1 hands
 //   the stripe's bottom row (HO, F) to lane 0 of the next stripe through a
-//   per-warp global scratch row (L2-resident);
+//   per-warp global scratch row (L2-resident, no per-column conditions);
 // * the argmax keeps, per lane and half, the first column where the lane's
 //   running max improved (strict >) plus the HO values of that column, and
 //   emits one 64-bit key (S, -j, -i) per lane with atomicMax -- the lexmin
@@ -53,7 +53,13 @@
 #define SW_BODY_BLOCKS 2   // 4-column blocks per unrolled loop body (forward; chosen by tools/gevo_search.py)
 #endif
 #ifndef SW_XFORM
-#define SW_XFORM 1         // clamped-E/F cell update with a one-op row chain (see sweep<>); 0: shifted-state update
+#define SW_XFORM 1         // 1: clamped-E/F update with a one-op row chain (four max operations, default);
+                           // 2: three-max update, additions on the FMA pipe, a three-op row chain (measured
+                           // slower: c2 forward 4.73 vs 4.90 TCUPS); 0: shifted-state update (see sweep<>)
+#endif
+#ifndef SW_IMPROVE_VOTE
+#define SW_IMPROVE_VOTE 0  // 1: non-TAG forward with a warp-uniform improvement branch (vote) + predicated per-half
+                           // stores (measured slower: c3 forward 3.14 vs 3.23 TCUPS, c5 3.63 vs 3.86)
 #endif
 #ifndef SW_PROT_T4
 #define SW_PROT_T4 1       // protein profile build from a transposed (s - o) table with byte transposes
@@ -254,7 +260,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
                                       const int mmax, const int row0, const uint32_t o2, const uint32_t e2, const int o,
                                       const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch,
-                                      const int scr_lim) {
+                                      const int scr_cols) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
@@ -369,8 +375,18 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 #pragma unroll
         for (int h = 0; h < NH; ++h)
             if (u < CD) cd[u][h] = ld_code(rp[h] + u);
-        if (MULTI) bnd[u] = (from_scratch && L == 0 && u < scr_lim) ? __ldcg(scr_in + u) : make_uint2(b0, 0u);
+        if (MULTI) bnd[u] = __ldcg(scr_in + u);
     }
+    // Stripe hand-off without per-column conditions: every lane of a segment loads lane 0's
+    // boundary word (one broadcast LDG), and an IMAD keeps it only where it applies -- lane 0 of
+    // a stripe below the first -- else the constant border b0 (lane 0 of the first stripe) or 0
+    // (the other lanes, which take the row above from the shuffle).  The producing stripe filled
+    // every column it did not sweep with the border (see the kernel), so no stale value is ever
+    // read; the store is predicated on a loop-invariant lane test into a row with W slots of slack
+    // before column 0.
+    const uint32_t useL0 = opaque((MULTI && from_scratch && L == 0) ? 1u : 0u);
+    const uint32_t bconst = (MULTI && from_scratch) ? 0u : b0;
+    const bool st_lane = MULTI && to_scratch && L == W - 1;
 
     // reverse pass: packed targets of both halves (the forward score S of each pair); the
     // TAG route compares block maxima against S*64 (0x7fff: half finished or empty)
@@ -440,11 +456,9 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             }
             uint32_t bHO = b0, bF = 0u;
             if (MULTI) {
-                bHO = bnd[u].x; bF = bnd[u].y;
-                // only the columns the previous stripe swept were handed off (scr_lim <= mmax):
-                // past them -- the item's longest reference, or where a reverse sweep stopped
-                // early -- the constant boundary, never a stale row (see the kernel below)
-                bnd[u] = (from_scratch && L == 0 && t + U < scr_lim) ? __ldcg(scr_in + t + U) : make_uint2(b0, 0u);
+                bHO = bnd[u].x * useL0 + bconst;  // IMAD (FMA pipe)
+                bF = bnd[u].y * useL0;
+                bnd[u] = __ldcg(scr_in + t + U);
             }
             // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
             const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
@@ -475,6 +489,26 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     xv = T::addmax_relu(hd, sc, HO[r]);
                     hd = HO[r];
                     HO[r] = T::add(T::max2(xv, hu), o2s);
+                    hu = HO[r];
+                } else if (SW_XFORM == 2) {
+                    // Three-max form (R = H + o kept per row, as below; E and F unclamped, bounded
+                    // below by o since R >= o):
+                    //   t        = R[i-1][j-1] + (s - o)                           VIADD.16x2 (FMA pipe)
+                    //   E[i][j]  = max(E[i][j-1] + e, R[i][j-1])                    VIADDMNMX
+                    //   F[i][j]  = max(F[i-1][j] + e, R[i-1][j])                    VIADDMNMX
+                    //   H[i][j]  = max(t, E, F, 0)                                  VIMNMX3.RELU
+                    //   R[i][j]  = H + o                                            VIADD.16x2 (FMA pipe)
+                    // which is the Gotoh recurrence of the header with the borders E = F = o or 0
+                    // (<= o - e, so they never win a max that matters: reading R13 / pin P13).  Three
+                    // ALU max operations per cell pair instead of four (the additions ride the FMA
+                    // pipe); the row chain is F -> H -> R (three operations).  The running max
+                    // tracks H itself (>= 0; its cells equal to S are those of X in the form below).
+                    const uint32_t tt = T::add(hd, sc);
+                    E[r] = T::addmax(E[r], e2, HO[r]);
+                    F = T::addmax(F, e2, hu);
+                    xv = T::max3(tt, E[r], F);
+                    hd = HO[r];
+                    HO[r] = T::add(xv, o2s);
                     hu = HO[r];
                 } else if (SW_XFORM) {
                     // E^ = max(E, 0), F^ = max(F, 0), X = max(H[i-1][j-1] + s, E^) (>= 0), R = H + o:
@@ -553,6 +587,20 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                         bc[h] = dh ? t - L : bc[h];
                     }
                     best = nb;
+                } else if (SW_IMPROVE_VOTE && SW_XFORM) {
+                    // warp-uniform branch (no divergence bookkeeping): when some lane's running max
+                    // improved, every lane issues predicated stores of the column for the halves
+                    // that improved and moves their column record
+                    const uint32_t d = nb ^ best;
+                    if (__any_sync(FULL, d != 0u)) {
+#pragma unroll
+                        for (int h = 0; h < NH; ++h) {
+                            const uint32_t dh = NH == 1 ? d : (h ? d >> 16 : d & 0xffffu);
+                            sv_store_if<K>(sv[h], H, dh);
+                            bc[h] = dh ? t - L : bc[h];
+                        }
+                    }
+                    best = nb;
                 } else if (nb != best) {
                     const uint32_t d = nb ^ best;
 #pragma unroll
@@ -579,10 +627,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 next_ev = ev[0];
                 if (NH == 2) next_ev = min(next_ev, ev[NH - 1]);
             }
-            if (MULTI && to_scratch && L == W - 1) {
-                const int c = t - (W - 1);
-                if (c >= 0 && c < mmax) scr_out[c] = make_uint2(hoLast, fLast);
-            }
+            if (st_lane) scr_out[t - (W - 1)] = make_uint2(hoLast, fLast);
         }
         if (TAG && !REV && (SW_TAG_LAZY || nbt != best)) tag_commit(nbt, t0);
         if (TAG && REV) {
@@ -602,6 +647,16 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     if (!REV && !EV) {
 #pragma unroll
         for (int h = 0; h < NH; ++h) emit(h);
+    }
+    if (MULTI && to_scratch) {
+        // Columns this sweep did not hand off (it wrote [-(W-1), t00 - W + 1)): the border, so the
+        // next stripe never reads a row left by an earlier item -- a reverse sweep stops early
+        // (reading R6) while the next stripe may still sweep further for another half of the item
+        // (the round-1 soak failure).  The border is a lower bound of the true
+        // row (H is monotone in it); it only feeds columns the early stop already settled or cells
+        // of a half's own rectangle / pad run, where H <= S.
+        __syncwarp();
+        for (int c = t00 - (W - 1) + L; c < scr_cols; c += W) scr_out[c] = make_uint2(R0, 0u);
     }
     return t00;  // column steps swept (statistics)
 }
@@ -862,17 +917,8 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             __syncwarp();
             if (lane < SLOTS) stop[lane] = 0x7fffffff;
         }
-        // Columns of the stripe boundary row the previous stripe handed off: lane W-1 writes column
-        // c at step c + W - 1, for every step the sweep ran, so a sweep of t_sw steps hands off
-        // columns [0, min(mmax, t_sw - W + 1)).  A reverse sweep stops early (reading R6) once
-        // every half found its start or ran out of columns, and the next stripe may need columns
-        // past that point (another half of the item still searching, or the 4-column TAG block of
-        // a start that lies up to 3 columns before them); those columns must not be read from the
-        // scratch row, which still holds an earlier item's values there.  They take the constant
-        // border instead: a lower bound of the true row (H is monotone in the border values), and
-        // every such cell lies right of the columns the early stop already settled, or past the
-        // half's reversed rectangle whose cells stay < S up to the REV_PAD pad codes.
-        int scr_lim = 0;
+        // stripe hand-off rows: W slots of slack before column 0, scr_cols columns after it
+        const int scr_cols = (int)(P.scratch_seg_bytes / (int64_t)sizeof(uint2)) - W;
         for (int s = 0; s < ns; ++s) {
             const int row0 = s * G::ROWS;
             // ---- build the stripe's query profile: (s - o) per (slot, code, lane, row) ----
@@ -984,18 +1030,15 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
                                                       row0, o2, e2, o, nullptr, nullptr, false, false, 0);
             } else {
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
-                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes);
+                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes) + W;
                 uint2* scr_out = reinterpret_cast<uint2*>(
-                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes);
-                int t_sw;
+                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes) + W;
                 if (need_ev)
-                    t_sw = sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                  row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_lim);
+                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                    row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_cols);
                 else
-                    t_sw = sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                   row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_lim);
-                steps += t_sw;
-                scr_lim = min(mmax, max(0, t_sw - (W - 1)));
+                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_cols);
             }
         }
         if (lane == 0) atomicAdd(P.swept, steps * G::ROWS * SLOTS);

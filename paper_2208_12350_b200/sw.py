@@ -332,7 +332,7 @@ class Aligner:
         import torch
         n = qo.numel() - 1
         if ops is None:
-            ops = torch.empty(int(q.numel() + r.numel()) + 1, dtype=torch.uint8, device=q.device)
+            ops = torch.zeros(int(q.numel() + r.numel()) + 1, dtype=torch.uint8, device=q.device)
         if n_ops is None:
             n_ops = torch.empty(max(n, 1), dtype=torch.int32, device=q.device)
         rr = sw_result_t(res[0].data_ptr(), res[1].data_ptr(), res[2].data_ptr(), res[3].data_ptr(), res[4].data_ptr())

@@ -11,7 +11,7 @@ from paper_2208_12350_b200 import sw, synth  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 npairs = int(sys.argv[2]) if len(sys.argv) > 2 else None
 t = time.time()
-b = synth.generate(cfg, 0, npairs)
+b = synth.generate_parallel(cfg, 0, npairs)
 print(f"gen {cfg} {b.n_pairs} pairs cells={b.cells():.3e} in {time.time()-t:.1f}s", flush=True)
 a = sw.Aligner(0)
 a.enable_stage_timing(True)
@@ -42,4 +42,4 @@ rsw = a.reverse_cells()
 print(f"rev swept cells = {rsw:.4g} ({rsw/max(fwd,1):.3f} of fwd real); rev kernel swept GCUPS = {rsw/st['rev']/1e6:.1f}; "
       f"fwd kernel swept GCUPS = {swept/st['fwd']/1e6:.1f}")
 print("launches:", a.launch_count(), "status:", a.batch_status())
-print("dpx peak TCUPS:", sw.sw_dpx_peak(0, 200.0) / 1e12)
+print("dpx peak TCUPS:", sw.sw_dpx_peak(0, 200.0) / 1e12, "lib:", __import__("os").environ.get("SW_B200_LIB", "default"))
