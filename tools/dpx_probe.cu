@@ -1,8 +1,9 @@
 // tools/dpx_probe.cu -- issue-rate probe for the integer/DPX instructions the
 // Smith-Waterman inner loop uses (VIADDMNMX.S16x2, VIMNMX(3).S16x2, VIADD,
 // PRMT, IMAD, LOP3, SHFL).  Standalone: nvcc -gencode arch=compute_100a,code=sm_100a.
-// Prints, per probe, warp-instructions issued per SM clock (clock64 based, so
-// independent of the SM frequency) and the wall-clock rate.
+// Prints, per probe, the event-timed warp-instruction rate of the whole GPU and that
+// rate per SM per cycle of the maximum SM clock (a lower bound of the per-cycle rate
+// when the clock runs below its maximum).
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -157,11 +158,14 @@ void run(int sms, int blocks_per_sm, int threads) {
     double cyc = 0; for (int w = 0; w < warps; ++w) cyc += h[w].cycles; cyc /= warps;
     double winstr_per_warp = INSTR_PER_CHAIN[V] * CHAINS * ITERS;
     int warps_per_sm = blocks_per_sm * threads / 32;
-    double ipc = winstr_per_warp * warps_per_sm / cyc;   // warp-instr / SM clock
+    (void)cyc;  // per-warp clock64 spans do not measure SM cycles (warps of a block are not all
+                // resident for the whole span): only the event-timed rate is reported
     double wall_rate = winstr_per_warp * warps / (ms * 1e-3);  // warp-instr / s (whole GPU)
-    double mhz = (cyc / (ms * 1e-3)) / 1e6;
-    printf("%-22s warps/SM=%2d  warp-instr/clk/SM=%.3f  GPU warp-instr/s=%.3e  implied SM MHz=%.0f  ms=%.3f\n",
-           NAMES[V], warps_per_sm, ipc, wall_rate, mhz, ms);
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
+    double per_clk = wall_rate / ((double)sms * khz * 1e3);  // at the maximum SM clock (event-timed)
+    printf("%-22s warps/SM=%2d  GPU warp-instr/s=%.3e  = %.3f warp-instr per SM per max-clock cycle  ms=%.3f\n",
+           NAMES[V], warps_per_sm, wall_rate, per_clk, ms);
     if (V == 0 || V == 5 || V == 6 || V == 12 || V == 13 || V == 17 || V == 18) {
         double cellpairs = (double)CHAINS * ITERS * 32.0 * warps;
         printf("    -> cell updates/s (2 cells per s16x2 chain step) = %.3f TCUPS\n", 2 * cellpairs / (ms * 1e-3) / 1e12);
