@@ -596,7 +596,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
     F.target = h->target.p; F.key_rev = h->key.p; F.hist = hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
     F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
-    F.out = *out; F.stats = stats; F.end_only = end_only ? 1 : 0;
+    F.out = *out; F.stats = stats; F.end_only = end_only ? 1 : 0; F.rev_small = small_rev ? 1 : 0;
     {
         const int64_t warps = std::min<int64_t>((hi - lo + FIN_PPW - 1) / FIN_PPW, (int64_t)h->sm_count * 64);
         finish_fwd_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(F);

@@ -26,6 +26,7 @@ struct FinishParams {
     int max_sigma, gap_extend;
     uint8_t pad_code;
     int end_only;                   // forward pass only: no start outputs, no reverse-pass preparation
+    int rev_small;                  // the reverse pass is counting-sorted on exact (stripes, columns) bins
     sw_result_t out;
     BatchStats* stats;
 };
@@ -111,9 +112,20 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                 P.nlen_rev[p] = n2;
                 P.mlen_rev[p] = m2;
                 P.target[p] = S;
-                // reverse work items are grouped by (stripes, S): the early-stopped sweep's length
-                // follows the alignment's span, for which S is the available proxy
-                const uint32_t key = work_key(route, stripes, (uint32_t)S);
+                // reverse work items are grouped by (stripes, columns per stripe): a single stripe's
+                // early-stopped sweep follows the alignment's span, for which S is the available
+                // proxy; a multi-stripe pair sweeps per stripe at most its band (sw_wavefront.cuh:
+                // columns [B - n2 + row0, m2 + r1 - B], B = ceil(S / max_s)), i.e. at most
+                // min(m2, n2 + m2 - 2B + rows) columns -- the estimate that keeps the longest items first
+                // An exact-bin (counting-sort) batch keeps (stripes, columns); a radix-sorted one -- long
+                // pairs -- orders multi-stripe items by their work, stripes x columns (in units of 256
+                // cells-rows), then columns: an unrelated long pair whose gapped score grows with its
+                // length (no narrow band) can outweigh a higher-identity pair with more stripes
+                const int B = (S + P.max_sigma - 1) / P.max_sigma;
+                const int band = max(1, (int)min((long long)m2, (long long)n2 + m2 - 2LL * B + rows));
+                const uint32_t key = stripes == 1 ? work_key(route, 1u, (uint32_t)S)
+                                   : P.rev_small ? work_key(route, stripes, (uint32_t)band)
+                                   : work_key(route, (uint32_t)min(0x3fffLL, ((long long)stripes * band) >> 8) + 1u, (uint32_t)band);
                 P.key_rev[p] = key;
                 const uint32_t bin = key_bin(key);
                 if (bin) atomicAdd(P.hist + bin, 1u);

@@ -46,6 +46,9 @@
 #include "sw_common.cuh"
 #include "sw_pack.cuh"
 
+#define SV_QSTRIDE 512u  // bytes between quads of a saved column (32 lanes x 16 B), see Geometry::SVH
+#define U_MAX_FILL 8     // >= the column unroll x loop-body blocks + the prefetch distance: the hand-off fill margin
+
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4
 #endif
@@ -134,6 +137,10 @@ struct Geometry {
     static constexpr int PB = (T::NH == 2) ? (K <= 4 ? 4 : K <= 8 ? 8 : 16 * ((K + 15) / 16)) : 16 * ((4 * K + 15) / 16);
     static constexpr int PWORDS = PB / 4;
     static constexpr int SVB = 16 * ((4 * K + 15) / 16);    // saved improvement column per (lane, half)
+    // saved columns are stored quad-major across the warp's lanes: quad w of (half h, lane l) at
+    // h * SVH + w * SV_QSTRIDE + l * 16, so a warp-wide STS.128 / LDS.128 touches 32 consecutive
+    // 16-byte chunks (no bank conflicts; a lane-major 64-96 B stride conflicts 4-way)
+    static constexpr int SVH = 32 * SVB;
     static __host__ __device__ int prof_bytes(int nc) { return SLOTS * nc * W * PB; }
     static constexpr int STOP_BYTES = 16 * ((SLOTS * 4 + 15) / 16);
     // shared memory per warp: profile + REV stop steps + saved improvement columns
@@ -185,13 +192,13 @@ template <int K>
 __device__ __forceinline__ void sv_store(uint32_t addr, const Quads<K>& HO) {
 #pragma unroll
     for (int w = 0; w < K / 4; ++w)
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr + 16 * w), "r"(HO.q[w].x), "r"(HO.q[w].y),
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" :: "r"(addr + SV_QSTRIDE * w), "r"(HO.q[w].x), "r"(HO.q[w].y),
                      "r"(HO.q[w].z), "r"(HO.q[w].w) : "memory");
     if (K % 4 >= 2)
-        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(addr + 16 * (K / 4)), "r"(HO.q[K / 4].x),
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" :: "r"(addr + SV_QSTRIDE * (K / 4)), "r"(HO.q[K / 4].x),
                      "r"(HO.q[K / 4].y) : "memory");
     if (K % 4 == 1 || K % 4 == 3)
-        asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr + 16 * (K / 4) + (K % 4 == 3 ? 8u : 0u)),
+        asm volatile("st.shared.u32 [%0], %1;" :: "r"(addr + SV_QSTRIDE * (K / 4) + (K % 4 == 3 ? 8u : 0u)),
                      "r"(K % 4 == 1 ? HO.q[K / 4].x : HO.q[K / 4].z) : "memory");
 }
 
@@ -209,14 +216,14 @@ __device__ __forceinline__ void sv_store_if(uint32_t addr, const uint32_t (&v)[K
 #pragma unroll
     for (int w = 0; w < K / 4; ++w)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t@p st.shared.v4.u32 [%0], {%1, %2, %3, %4};\n\t}"
-                     :: "r"(addr + 16 * w), "r"(v[4 * w]), "r"(v[4 * w + 1]), "r"(v[4 * w + 2]), "r"(v[4 * w + 3]),
+                     :: "r"(addr + SV_QSTRIDE * w), "r"(v[4 * w]), "r"(v[4 * w + 1]), "r"(v[4 * w + 2]), "r"(v[4 * w + 3]),
                      "r"(cond) : "memory");
     if (K % 4 >= 2)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t@p st.shared.v2.u32 [%0], {%1, %2};\n\t}"
-                     :: "r"(addr + 16 * (K / 4)), "r"(v[4 * (K / 4)]), "r"(v[4 * (K / 4) + 1]), "r"(cond) : "memory");
+                     :: "r"(addr + SV_QSTRIDE * (K / 4)), "r"(v[4 * (K / 4)]), "r"(v[4 * (K / 4) + 1]), "r"(cond) : "memory");
     if (K % 4 == 1 || K % 4 == 3)
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %1;\n\t}"
-                     :: "r"(addr + 16 * (K / 4) + (K % 4 == 3 ? 8u : 0u)), "r"(v[K - 1]), "r"(cond) : "memory");
+                     :: "r"(addr + SV_QSTRIDE * (K / 4) + (K % 4 == 3 ? 8u : 0u)), "r"(v[K - 1]), "r"(cond) : "memory");
 }
 
 // First row r of the saved column whose half h equals `target` (an HO value).
@@ -225,7 +232,7 @@ __device__ __forceinline__ int sv_first_row(uint32_t addr, int h, int target) {
     int rr = 0;
 #pragma unroll
     for (int w = (K + 3) / 4 - 1; w >= 0; --w) {
-        const uint4 v = lds128(addr + 16 * w);
+        const uint4 v = lds128(addr + SV_QSTRIDE * w);
         const uint32_t x[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int b = 3; b >= 0; --b)
@@ -256,11 +263,11 @@ __device__ __forceinline__ uint4 lds_rem(uint32_t addr) {
 // reference are pad codes, whose cells stay below S).
 template <class T, int W, int K, bool REV, bool MULTI, bool EV, bool TAG, bool LIN>
 __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, volatile int* stop, const uint32_t sv_base,
-                                      const int seg, const int L, const int s_m, const int (&h_pid)[T::NH],
+                                      const int seg, const int L, const int s_lim, const int (&h_pid)[T::NH],
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
                                       const int mmax, const int row0, const uint32_t o2, const uint32_t e2, const int o,
                                       const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch,
-                                      const int scr_cols) {
+                                      const int scr_cols, const int c_lo) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
@@ -303,17 +310,20 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
         brow[h] = 0;
         bt0[h] = 0;
         btag[h] = 0u;
-        sv[h] = sv_base + (uint32_t)h * G::SVB;
+        sv[h] = sv_base + (uint32_t)h * G::SVH;
         ev[h] = (EV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
         next_ev = min(next_ev, ev[h]);
     }
+    // diagonal input of lane 0's first column: the left border, or -- for a reverse stripe that starts
+    // at c_lo > 0 -- the previous stripe's bottom row at column c_lo - 1 (inside that row's band)
     uint32_t hoLast = R0, fLast = 0u, prevUpHO = R0;
+    if (MULTI && from_scratch && L == 0 && c_lo > 0) prevUpHO = __ldcg(scr_in - 1).x;
     uint32_t prof_h[NH];  // shared-window address of this lane's profile entries, code 0
     const uint8_t* rp[NH];
 #pragma unroll
     for (int h = 0; h < NH; ++h) {
         prof_h[h] = (uint32_t)__cvta_generic_to_shared(prof + (size_t)(seg * NH + h) * nc * CS + (size_t)L * G::PB);
-        rp[h] = P.rcode + h_rpos[h] - L;  // this lane's column 0 (pad codes before it)
+        rp[h] = P.rcode + h_rpos[h] - L + c_lo;  // this lane's first column c_lo (pad codes before column 0)
     }
     const uint32_t cs = opaque(CS);  // code stride as a runtime value: the address is one IMAD
     // lane 0 takes the row above from the stripe boundary: up = shfl * notL0 + b (IMAD)
@@ -407,9 +417,9 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             const int v = T::get(nbt_, h);
             if (v >= T::get(tgt64, h)) {
                 const int col = t0 + (U - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
-                if ((v >> 6) == h_tgt[h] && col < h_m[h]) {
-                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], col, row0 + L * K + ((1 << RB) - 1) - (v & ((1 << RB) - 1))));
-                    atomicMin((int*)stop + seg * NH + h, col + W);
+                if ((v >> 6) == h_tgt[h] && col + c_lo < h_m[h]) {
+                    atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], col + c_lo, row0 + L * K + ((1 << RB) - 1) - (v & ((1 << RB) - 1))));
+                    atomicMin((int*)stop + seg * NH + h, col + c_lo + W);
                 }
                 tgt64 = T::set(tgt64, h, 0x7fff);
                 found_blk = 1;
@@ -418,10 +428,12 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     };
     int T_end = mmax + W - 1;
     if (REV) {
+        // steps until every lane passed each slot's last needed column (its reversed reference, its
+        // band, or its found start: stop), in steps from column c_lo
         int te = 0;
 #pragma unroll
-        for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_m, sl) + W - 1, stop[sl]));
-        T_end = te;
+        for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_lim, sl), stop[sl]));
+        T_end = te - c_lo;
     }
     // NB blocks of U columns per loop iteration (the longer body lets ptxas keep loop-carried
     // values in place); tag bookkeeping stays per U-column block
@@ -567,8 +579,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                                 const uint32_t msk = NH == 1 ? 0xffffffffu : (h ? 0xffff0000u : 0x0000ffffu);
 #pragma unroll
                                 for (int r = K - 1; r >= 0; --r) if (((H[r] ^ tw) & msk) == 0u) rr = r;
-                                atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L, row0 + L * K + rr));
-                                atomicMin((int*)stop + seg * NH + h, t - L + W);
+                                atomicMax(P.keys + h_pid[h], pack_key(h_tgt[h], t - L + c_lo, row0 + L * K + rr));
+                                atomicMin((int*)stop + seg * NH + h, t - L + c_lo + W);
                                 tgt2 = T::set(tgt2, h, -1);
                                 found_blk = 1;
                             }
@@ -638,8 +650,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             __syncwarp();
             int te = 0;
 #pragma unroll
-            for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_m, sl) + W - 1, stop[sl]));
-            T_end = te;
+            for (int sl = 0; sl < SLOTS; ++sl) te = max(te, min(__shfl_sync(FULL, s_lim, sl), stop[sl]));
+            T_end = te - c_lo;
             found_blk = 0;
         }
       }
@@ -856,7 +868,7 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
     uint8_t* prof = smem + (size_t)warp * G::warp_smem(nc);
     volatile int* stop = reinterpret_cast<volatile int*>(prof + G::prof_bytes(nc));
     const uint32_t sv_base = (uint32_t)__cvta_generic_to_shared(prof + G::prof_bytes(nc) + G::STOP_BYTES) +
-                             (uint32_t)(lane * NH * G::SVB);
+                             (uint32_t)(lane * 16);
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
     const int n_path = P.counts[P.route];
@@ -921,6 +933,44 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
         const int scr_cols = (int)(P.scratch_seg_bytes / (int64_t)sizeof(uint2)) - W;
         for (int s = 0; s < ns; ++s) {
             const int row0 = s * G::ROWS;
+            // Reverse pass, stripes below the first: the exact band of the reversed rectangle.  A
+            // reversed alignment ending in cell (i', j') scores <= max_s * min(i' + 1, j' + 1), and
+            // from there to the start cell it can gain <= max_s * min(n2 - 1 - i', m2 - 1 - j'); every
+            // cell of a score-S path from the origin (and every cell holding S) therefore has
+            //   min(i' + 1, j' + 1) + min(n2 - 1 - i', m2 - 1 - j') >= B = ceil(S / max_s),
+            // which in rows [row0, r1] bounds the columns to [B - n2 + row0, m2 + r1 - B].  Cells
+            // outside are not swept: the stripe starts at the smallest such column of the item's
+            // halves with the border (H = 0) on its left, and each half's sweep ends at its largest.
+            // The swept cells then hold lower bounds of H' that are exact on every such path, so the
+            // cells with H' = S -- and their lexmin -- are unchanged (reading R6).
+            // A long, high-identity alignment (S close to max_s * n2, C5) sweeps a diagonal band of
+            // ~(n2 - B) columns per side instead of the whole rectangle.
+            int c_lo = 0, s_lim = s_m + W - 1;
+            // columns the next stripe can read from this stripe's hand-off row (absolute, exclusive)
+            int next_lim = mmax + W - 1;
+            if (REV) {
+                int lo = 0x7fffffff, nl = 0;
+                if (lane < SLOTS && s_pid >= 0) {
+                    const int ms = P.sc.max_sigma;
+                    const int B = (s_tgt + ms - 1) / ms;
+                    if (row0 >= s_n) {
+                        s_lim = 0;  // no row of this half in the stripe
+                    } else {
+                        const int r1 = min(row0 + G::ROWS, s_n) - 1;
+                        lo = max(0, B - s_n + row0);
+                        s_lim = min(s_m, s_m + r1 - B + 1) + W - 1;
+                    }
+                    if (row0 + G::ROWS < s_n)
+                        nl = min(s_m, s_m + min(row0 + 2 * G::ROWS, s_n) - B) + W - 1;
+                }
+#pragma unroll
+                for (int d = 16; d >= 1; d >>= 1) {
+                    lo = min(lo, __shfl_xor_sync(FULL, lo, d));
+                    nl = max(nl, __shfl_xor_sync(FULL, nl, d));
+                }
+                c_lo = lo == 0x7fffffff ? 0 : lo;
+                next_lim = nl;
+            }
             // ---- build the stripe's query profile: (s - o) per (slot, code, lane, row) ----
             __syncwarp();
             {
@@ -1023,22 +1073,25 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             if (swept) {
             } else if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, false, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                     row0, o2, e2, o, nullptr, nullptr, false, false, 0);
+                    steps += sweep<T, W, K, REV, false, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                     row0, o2, e2, o, nullptr, nullptr, false, false, 0, 0);
                 else
-                    steps += sweep<T, W, K, REV, false, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                      row0, o2, e2, o, nullptr, nullptr, false, false, 0);
+                    steps += sweep<T, W, K, REV, false, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                      row0, o2, e2, o, nullptr, nullptr, false, false, 0, 0);
             } else {
+                // rows in absolute columns (W slots of slack before column 0), seen from column c_lo
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
-                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes) + W;
+                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes) + W + c_lo;
                 uint2* scr_out = reinterpret_cast<uint2*>(
-                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes) + W;
+                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes) + W + c_lo;
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                    row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_cols);
+                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                    row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns,
+                                                    min(scr_cols, next_lim + 4 * U_MAX_FILL) - c_lo, c_lo);
                 else
-                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_m, h_pid, h_m, h_tgt, h_rpos, mmax,
-                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns, scr_cols);
+                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns,
+                                                    min(scr_cols, next_lim + 4 * U_MAX_FILL) - c_lo, c_lo);
             }
         }
         if (lane == 0) atomicAdd(P.swept, steps * G::ROWS * SLOTS);

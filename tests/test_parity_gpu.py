@@ -807,3 +807,44 @@ def test_reserved_call_rejects_batches_beyond_the_reservation():
         assert_parity(a.align(small), oracle_batch(small), small)
     finally:
         a.close()
+
+
+@pytest.mark.parametrize("kind", ["high_identity", "tandem_repeats", "protein_long"])
+def test_reverse_band_multistripe(aligner, kind):
+    """Reverse pass of multi-stripe pairs sweeps only the exact band min(i'+1, j'+1) + min(n2-1-i',
+    m2-1-j') >= ceil(S / max_s) below its first stripe (sw_wavefront.cuh): long high-identity
+    alignments (narrow band), tandem repeats (many optimal alignments on shifted diagonals: ties
+    between starts at the band's edges) and long protein pairs, all five fields vs the oracle."""
+    rng = np.random.default_rng({"high_identity": 31, "tandem_repeats": 32, "protein_long": 33}[kind])
+    pairs = []
+    if kind == "protein_long":
+        alpha = list("ARNDCQEGHILKMFPSTWYV")
+        sc = synth.PROTEIN_SCORING
+        for _ in range(24):
+            n = int(rng.integers(300, 1400))
+            q = rng.choice(alpha, n)
+            r = q.copy()
+            mut = rng.random(n) < rng.choice([0.0, 0.05, 0.3])
+            r[mut] = rng.choice(alpha, int(mut.sum()))
+            pre = "".join(rng.choice(alpha, int(rng.integers(0, 300))))
+            pairs.append(("".join(q), pre + "".join(r) + "".join(rng.choice(alpha, int(rng.integers(0, 300))))))
+    else:
+        sc = {"alphabet": "dna", "match": 2, "mismatch": -3, "gap_open": -5, "gap_extend": -2}
+        for _ in range(24):
+            n = int(rng.integers(330, 1500))
+            if kind == "tandem_repeats":
+                unit = "".join(rng.choice(list("ACGT"), int(rng.integers(1, 7))))
+                q = (unit * (n // len(unit) + 1))[:n]
+                r = (unit * ((n + 200) // len(unit) + 1))[: n + int(rng.integers(-50, 200))]
+            else:
+                qa = rng.choice(list("ACGT"), n)
+                ra = qa.copy()
+                mut = rng.random(n) < rng.choice([0.0, 0.01, 0.03])
+                ra[mut] = rng.choice(list("ACGT"), int(mut.sum()))
+                q = "".join(qa)
+                r = "".join(rng.choice(list("ACGT"), int(rng.integers(0, 400)))) + "".join(ra) + \
+                    "".join(rng.choice(list("ACGT"), int(rng.integers(0, 400))))
+            pairs.append((q, r))
+    b = synth.from_pairs(pairs, sc)
+    assert_parity(aligner.align(b), oracle_batch(b), b)
+    assert aligner.batch_status()[0] == sw.SW_OK
