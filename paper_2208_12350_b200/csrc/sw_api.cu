@@ -97,6 +97,7 @@ struct sw_context {
     // on two streams (slot k & 1), so their small kernels and tails overlap; slot 0 is the
     // device entry point's.
     DevBuf<uint8_t> scratch[N_SLOTS], cub_temp[N_SLOTS];
+    DevBuf<unsigned long long> progress[N_SLOTS];  // cooperative reverse items: per (warp, parity) hand-off progress
     BatchStats* d_stats = nullptr;  // [N_SLOTS]
     BatchStats* h_stats = nullptr;  // [N_SLOTS] (pinned)
     int64_t* h_ext = nullptr;
@@ -542,6 +543,11 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     int64_t seg_bytes = 0;
     {
         const size_t need = scratch_bytes(lf, lr, hs, protein, seg_bytes);
+        if (need) {
+            size_t wmax = 0;
+            for (int r = 0; r < N_ROUTES; ++r) wmax = std::max(wmax, (size_t)lr[r].blocks * lr[r].warps);
+            ENS(progress[slot], 2 * wmax);
+        }
         if (need && h->scratch[slot].cap < need) {
             ENS(scratch[slot], need);
             // defined contents: the first stripe of an item loads (and discards) its row
@@ -574,6 +580,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (!spec_bin) SW_CUDA(h, cudaMemsetAsync(counters, 0, 8 * sizeof(int32_t), s));
     WaveParams W;
     W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch[slot].p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
+    W.progress = h->progress[slot].p;
     W.tag_mul = 64;
     W.one = 1;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p + lo;
@@ -614,7 +621,9 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     if (st != SW_OK) return st;
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[5], s));
 
-    // 8. reverse wavefront on the reversed prefixes
+    // 8. reverse wavefront on the reversed prefixes (cooperative items' progress words start at 0)
+    if (seg_bytes && h->progress[slot].p)
+        SW_CUDA(h, cudaMemsetAsync(h->progress[slot].p, 0, h->progress[slot].cap * sizeof(unsigned long long), s));
     W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p + lo;
     W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &stats->swept_rev; W.counts = stats->rev_count;
     for (int r = 0; r < N_ROUTES; ++r) {
@@ -774,6 +783,8 @@ sw_status_t sw_reserve(sw_handle_t h, int64_t max_pairs, int64_t max_query_bytes
         st = ensure(h, h->scratch[0], need);
         if (st != SW_OK) return st;
         SW_CUDA(h, cudaMemset(h->scratch[0].p, 0, h->scratch[0].cap));
+        st = ensure(h, h->progress[0], (size_t)h->sm_count * 64 * 2);  // every resident warp, two rows
+        if (st != SW_OK) return st;
     }
     SW_CUDA(h, cudaDeviceSynchronize());
     h->res_pairs = max_pairs; h->res_qbytes = max_query_bytes; h->res_rbytes = max_ref_bytes;
@@ -1137,7 +1148,7 @@ sw_status_t sw_free(sw_handle_t h) {
     release(h->nlen); release(h->mlen); release(h->nlen_rev); release(h->mlen_rev); release(h->target);
     release(h->iota); release(h->order); release(h->order_rev); release(h->qpos); release(h->rpos); release(h->flags);
     release(h->key); release(h->key_sorted);
-    for (int k = 0; k < N_SLOTS; ++k) { release(h->cub_temp[k]); release(h->scratch[k]); } release(h->keys_fwd); release(h->keys_rev);
+    for (int k = 0; k < N_SLOTS; ++k) { release(h->cub_temp[k]); release(h->scratch[k]); release(h->progress[k]); } release(h->keys_fwd); release(h->keys_rev);
     release(h->qcode); release(h->rcode); release(h->rrev);
     release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
     release(h->db_q); release(h->db_qo);
@@ -1239,6 +1250,19 @@ sw_status_t sw_last_reverse_cells(sw_handle_t h, int64_t* swept) {
     *swept = (int64_t)t.swept_rev;
     return SW_OK;
 }
+
+#if SW_TRACE_ITEMS
+// development builds only: copy the per-item trace out (and reset it); returns the entry count
+int64_t sw_debug_item_trace(unsigned long long* host, int64_t max_entries) {
+    unsigned n = 0;
+    if (cudaMemcpyFromSymbol(&n, swb::g_trace_n, sizeof(n)) != cudaSuccess) return -1;
+    const int64_t k = std::min<int64_t>(std::min<int64_t>(n, swb::TRACE_CAP), max_entries);
+    if (host && k > 0 && cudaMemcpyFromSymbol(host, swb::g_trace, (size_t)k * 32) != cudaSuccess) return -1;
+    unsigned z = 0;
+    cudaMemcpyToSymbol(swb::g_trace_n, &z, sizeof(z));
+    return k;
+}
+#endif
 
 sw_status_t sw_dpx_peak(int device, double milliseconds, double* cups, void* stream) {
     if (!cups) return SW_ERR_INVALID_ARGUMENT;

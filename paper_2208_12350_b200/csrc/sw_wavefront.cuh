@@ -48,6 +48,10 @@
 
 #define SV_QSTRIDE 512u  // bytes between quads of a saved column (32 lanes x 16 B), see Geometry::SVH
 #define U_MAX_FILL 8     // >= the column unroll x loop-body blocks + the prefetch distance: the hand-off fill margin
+#ifndef SW_COOP_STRIPES
+#define SW_COOP_STRIPES 8  // reverse items with at least this many stripes are swept by all warps of a CTA
+#endif
+#define COOP_PUBLISH 32    // a cooperative producer publishes its hand-off progress every 32 column steps
 
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4
@@ -105,6 +109,20 @@
 
 namespace swb {
 
+#ifndef SW_TRACE_ITEMS
+#define SW_TRACE_ITEMS 0   // development builds only: per-item (route, pass, smid, start/end globaltimer, steps)
+#endif
+#if SW_TRACE_ITEMS
+constexpr int TRACE_CAP = 1 << 21;
+__device__ unsigned long long g_trace[TRACE_CAP][4];
+__device__ unsigned int g_trace_n;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 struct WaveParams {
     const uint8_t* qcode;       // query codes (positions qpos[p]; the reverse pass reads rows n-1 .. 0)
     const uint8_t* rcode;       // reference codes (padded positions rpos[p])
@@ -120,6 +138,7 @@ struct WaveParams {
     int32_t* item_counter;      // work queue head (zeroed before launch)
     uint8_t* scratch;           // stripe hand-off rows
     int64_t scratch_seg_bytes;  // bytes of one segment x parity buffer
+    unsigned long long* progress;  // per (warp, parity) hand-off row: CTA-cooperative reverse items (zeroed per call)
     unsigned long long* swept;  // cells swept (statistics)
     uint32_t tag_mul;           // = 64; a kernel parameter so the row tag is an IMAD (FMA pipe), not a LEA
     uint32_t one;               // = 1; a kernel parameter so H = Hb + o is an IMAD (FMA pipe), not an IADD3
@@ -267,7 +286,9 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                                       const int (&h_m)[T::NH], const int (&h_tgt)[T::NH], const int64_t (&h_rpos)[T::NH],
                                       const int mmax, const int row0, const uint32_t o2, const uint32_t e2, const int o,
                                       const uint2* scr_in, uint2* scr_out, const bool from_scratch, const bool to_scratch,
-                                      const int scr_cols, const int c_lo) {
+                                      const int scr_cols, const int c_lo,
+                                      const volatile unsigned long long* flag_in = nullptr, unsigned long long need_base = 0,
+                                      volatile unsigned long long* flag_out = nullptr, unsigned long long pub_base = 0) {
     using G = Geometry<W, K, T>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
@@ -314,10 +335,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
         ev[h] = (EV && h_pid[h] >= 0) ? L + h_m[h] - 1 : 0x7fffffff;
         next_ev = min(next_ev, ev[h]);
     }
-    // diagonal input of lane 0's first column: the left border, or -- for a reverse stripe that starts
-    // at c_lo > 0 -- the previous stripe's bottom row at column c_lo - 1 (inside that row's band)
     uint32_t hoLast = R0, fLast = 0u, prevUpHO = R0;
-    if (MULTI && from_scratch && L == 0 && c_lo > 0) prevUpHO = __ldcg(scr_in - 1).x;
     uint32_t prof_h[NH];  // shared-window address of this lane's profile entries, code 0
     const uint8_t* rp[NH];
 #pragma unroll
@@ -380,6 +398,25 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     static_assert(U % CD == 0, "SW_CODE_DIST must divide the column unroll");
     uint32_t cd[CD][NH];
     uint2 bnd[U];
+    // CTA-cooperative reverse item: the previous stripe's producer (another warp) publishes how many
+    // columns of its hand-off row are written (absolute, exclusive) with release semantics; this
+    // warp waits before loading columns it has not published (see the kernel)
+    unsigned long long seen = 0;
+    auto wait_cols = [&](int col_excl) {
+        if (MULTI && flag_in) {
+            const unsigned long long need = need_base | (unsigned long long)min(col_excl, 0x1fffff);
+            if (seen < need) {
+                do {
+                    seen = *flag_in;
+                } while (seen < need);
+                __threadfence();  // acquire: the row is read after the flag
+            }
+        }
+    };
+    wait_cols(c_lo + U);
+    // diagonal input of lane 0's first column: the left border, or -- for a reverse stripe that starts
+    // at c_lo > 0 -- the previous stripe's bottom row at column c_lo - 1 (inside that row's band)
+    if (MULTI && from_scratch && L == 0 && c_lo > 0) prevUpHO = __ldcg(scr_in - 1).x;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll
@@ -440,6 +477,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     constexpr int NB = REV ? SW_REV_BODY_BLOCKS : SW_BODY_BLOCKS;
     int t00 = 0;
     for (; t00 < T_end; t00 += U * NB) {
+      wait_cols(c_lo + t00 + U * NB + U);
 #pragma unroll
       for (int bb = 0; bb < NB; ++bb) {
         const int t0 = t00 + bb * U;
@@ -501,6 +539,24 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     xv = T::addmax_relu(hd, sc, HO[r]);
                     hd = HO[r];
                     HO[r] = T::add(T::max2(xv, hu), o2s);
+                    hu = HO[r];
+                } else if (SW_XFORM == 3) {
+                    // Three-max form with a two-operation row chain: F of the row below is formed as
+                    // soon as H of this row exists, max(H + o, F + e), with F + e added off the chain
+                    //   t        = R[i-1][j-1] + (s - o)                           VIADD.16x2 (FMA pipe)
+                    //   E[i][j]  = max(E[i][j-1] + e, R[i][j-1])                    VIADDMNMX
+                    //   H[i][j]  = max(t, E, F[i][j], 0)                            VIMNMX3.RELU
+                    //   F[i+1][j] = max(H[i][j] + o, F[i][j] + e)                   VIADDMNMX (+ VIADD, FMA)
+                    //   R[i][j]  = H + o                                            VIADD.16x2 (FMA pipe)
+                    // F of the lane's first row is max(F_up + e, R_up) as in the forms below; F keeps
+                    // the last row's value for the hand-off (the next lane forms its first row's F).
+                    const uint32_t tt = T::add(hd, sc);
+                    E[r] = T::addmax(E[r], e2, HO[r]);
+                    if (r == 0) F = T::addmax(F, e2, hu);
+                    xv = T::max3(tt, E[r], F);
+                    if (r + 1 < K) F = T::addmax(xv, o2s, T::add(F, e2));
+                    hd = HO[r];
+                    HO[r] = T::add(xv, o2s);
                     hu = HO[r];
                 } else if (SW_XFORM == 2) {
                     // Three-max form (R = H + o kept per row, as below; E and F unclamped, bounded
@@ -646,6 +702,13 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             const uint32_t x = T::max2(nbt, tgt64) ^ nbt;  // zero half: block max >= S*64
             if (((x - 0x00010001u) & ~x & 0x80008000u) != 0u) rev_tag_find(nbt, t0);
         }
+        if (MULTI && flag_out && ((t0 + U) % COOP_PUBLISH) == 0) {
+            // release: this stripe's row is written up to column c_lo + t0 + U - W + 1 (exclusive)
+            __threadfence();
+            __syncwarp();
+            __threadfence();
+            if (L == 0 && seg == 0) *flag_out = pub_base | (unsigned long long)max(0, c_lo + t0 + U - W + 1);
+        }
         if (REV && __any_sync(FULL, found_blk)) {  // re-read the stop columns only after a find
             __syncwarp();
             int te = 0;
@@ -669,6 +732,12 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
         // of a half's own rectangle / pad run, where H <= S.
         __syncwarp();
         for (int c = t00 - (W - 1) + L; c < scr_cols; c += W) scr_out[c] = make_uint2(R0, 0u);
+        if (flag_out) {  // the whole row (swept and border-filled) is readable
+            __threadfence();
+            __syncwarp();
+            __threadfence();
+            if (L == 0 && seg == 0) *flag_out = pub_base | 0x1fffffull;
+        }
     }
     return t00;  // column steps swept (statistics)
 }
@@ -879,12 +948,12 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
     const uint32_t e2 = T::splat(P.sc.gap_extend);
     const int o = P.sc.gap_open;
 
-    for (;;) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(P.item_counter, 1);
-        item = __shfl_sync(FULL, item, 0);
-        if (item >= items) break;
-
+    // One work item (SLOTS pairs) swept by `npart` warps of the CTA: warp `part` takes stripes part,
+    // part + npart, ... (npart = 1: this warp alone).  stop_i: the item's per-slot stop columns.
+    auto run_item = [&](const int item, const int part, const int npart, volatile int* stop_i) {
+#if SW_TRACE_ITEMS
+        const unsigned long long tr_t0 = gtimer();
+#endif
         // ---- slot descriptors (lane s < SLOTS holds slot s) ----
         int s_pid = -1, s_n = 0, s_m = 0, s_tgt = 0;
         int64_t s_rpos = 0, s_qpos = 0;
@@ -925,13 +994,13 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
         }
         unsigned long long steps = 0;  // column steps over the item's stripes
 
-        if (REV) {
+        if (REV && npart == 1) {
             __syncwarp();
-            if (lane < SLOTS) stop[lane] = 0x7fffffff;
+            if (lane < SLOTS) stop_i[lane] = 0x7fffffff;
         }
         // stripe hand-off rows: W slots of slack before column 0, scr_cols columns after it
         const int scr_cols = (int)(P.scratch_seg_bytes / (int64_t)sizeof(uint2)) - W;
-        for (int s = 0; s < ns; ++s) {
+        for (int s = part; s < ns; s += npart) {
             const int row0 = s * G::ROWS;
             // Reverse pass, stripes below the first: the exact band of the reversed rectangle.  A
             // reversed alignment ending in cell (i', j') scores <= max_s * min(i' + 1, j' + 1), and
@@ -1073,28 +1142,103 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
             if (swept) {
             } else if (SW_SINGLE_ONLY || ns == 1) {
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, false, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, true, TAGF, LIN>(P, prof, stop_i, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, nullptr, nullptr, false, false, 0, 0);
                 else
-                    steps += sweep<T, W, K, REV, false, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, false, false, TAGF, LIN>(P, prof, stop_i, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                       row0, o2, e2, o, nullptr, nullptr, false, false, 0, 0);
             } else {
-                // rows in absolute columns (W slots of slack before column 0), seen from column c_lo
+                // rows in absolute columns (W slots of slack before column 0), seen from column c_lo.
+                // Stripe s writes the row of warp (s mod npart) of the CTA (this warp), parity
+                // (s / npart) & 1, and reads its predecessor's; cooperative items (npart > 1) order
+                // the two with a progress word per row (the producer is another warp)
+                const int wbase = gwarp - warp;  // the CTA's first warp
+                const int pw = (s + npart - 1) % npart, pp = ((s - 1) / npart) & 1;  // s >= 1 only
+                const int ow = s % npart, op = (s / npart) & 1;
                 const uint2* scr_in = reinterpret_cast<const uint2*>(
-                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + (s & 1)) * P.scratch_seg_bytes) + W + c_lo;
+                    P.scratch + ((size_t)(npart > 1 ? wbase + pw : gwarp) * G::SEGS * 2 + seg * 2 + (npart > 1 ? pp : ((s + 1) & 1))) *
+                                    P.scratch_seg_bytes) + W + c_lo;
                 uint2* scr_out = reinterpret_cast<uint2*>(
-                    P.scratch + ((size_t)gwarp * G::SEGS * 2 + seg * 2 + ((s + 1) & 1)) * P.scratch_seg_bytes) + W + c_lo;
+                    P.scratch + ((size_t)(npart > 1 ? wbase + ow : gwarp) * G::SEGS * 2 + seg * 2 + (npart > 1 ? op : (s & 1))) *
+                                    P.scratch_seg_bytes) + W + c_lo;
+                const volatile unsigned long long* f_in =
+                    (npart > 1 && s > 0) ? P.progress + (size_t)(wbase + pw) * 2 + pp : nullptr;
+                volatile unsigned long long* f_out = (npart > 1 && s + 1 < ns) ? P.progress + (size_t)(wbase + ow) * 2 + op : nullptr;
+                // progress words: (route, item + 1, stripe, columns): monotonic over the launches of a
+                // call (routes in order) and the items a CTA takes; zeroed per call
+                const unsigned long long tag_item = ((unsigned long long)P.route << 61) | ((unsigned long long)(item + 1) << 32);
+                const unsigned long long nb_in = tag_item | ((unsigned long long)(s - 1) << 21);
+                const unsigned long long nb_out = tag_item | ((unsigned long long)s << 21);
                 if (need_ev)
-                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, true, TAGF, LIN>(P, prof, stop_i, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                     row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns,
-                                                    min(scr_cols, next_lim + 4 * U_MAX_FILL) - c_lo, c_lo);
+                                                    min(scr_cols, next_lim + 4 * U_MAX_FILL) - c_lo, c_lo, f_in, nb_in, f_out, nb_out);
                 else
-                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
+                    steps += sweep<T, W, K, REV, true, false, TAGF, LIN>(P, prof, stop_i, sv_base, seg, L, s_lim, h_pid, h_m, h_tgt, h_rpos, mmax,
                                                      row0, o2, e2, o, scr_in, scr_out, s > 0, s + 1 < ns,
-                                                    min(scr_cols, next_lim + 4 * U_MAX_FILL) - c_lo, c_lo);
+                                                    min(scr_cols, next_lim + 4 * U_MAX_FILL) - c_lo, c_lo, f_in, nb_in, f_out, nb_out);
             }
         }
         if (lane == 0) atomicAdd(P.swept, steps * G::ROWS * SLOTS);
+#if SW_TRACE_ITEMS
+        if (lane == 0 && part == 0) {
+            const unsigned k = atomicAdd(&g_trace_n, 1u);
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            if (k < (unsigned)TRACE_CAP) {
+                g_trace[k][0] = ((unsigned long long)item << 32) | ((unsigned long long)smid << 16) | ((REV ? 1u : 0u) << 8) | (unsigned)P.route;
+                g_trace[k][1] = tr_t0;
+                g_trace[k][2] = gtimer();
+                g_trace[k][3] = ((unsigned long long)ns << 48) | ((unsigned long long)(unsigned)mmax << 24) | (steps & 0xffffffull);
+            }
+        }
+#endif
+    };
+
+    // stripes of an item (warp-uniform): the longest query of its slots
+    auto item_stripes = [&](const int item) -> int {
+        int n = 0;
+        if (lane < SLOTS) {
+            const int idx = item * SLOTS + lane;
+            if (idx < n_path) n = P.nlen[P.order[first + idx]];
+        }
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) n = max(n, __shfl_xor_sync(FULL, n, d));
+        return (n + G::ROWS - 1) / G::ROWS;
+    };
+
+    if constexpr (REV) {
+        // Reverse pass: the longest items come first in the queue.  While they have at least
+        // SW_COOP_STRIPES stripes, a CTA takes one item at a time and all its warps sweep it together,
+        // consecutive stripes on consecutive warps, each stripe lagging its predecessor by a publish
+        // interval -- one item no longer runs for the length of the whole pass on one warp (the
+        // tail of long unrelated pairs, whose start lies far from the origin).
+        // The first shorter item ends the phase: warp 0 sweeps it and every warp continues alone.
+        __shared__ int s_item;
+        const int nwarps = blockDim.x >> 5;
+        if (nwarps > 1) {
+            volatile int* stop0 = reinterpret_cast<volatile int*>(smem + G::prof_bytes(nc));  // warp 0's
+            for (;;) {
+                __syncthreads();
+                if (threadIdx.x == 0) s_item = atomicAdd(P.item_counter, 1);
+                if (warp == 0 && lane < SLOTS) stop0[lane] = 0x7fffffff;
+                __syncthreads();
+                const int item = s_item;
+                if (item >= items) return;
+                if (item_stripes(item) < SW_COOP_STRIPES) {
+                    if (warp == 0) run_item(item, 0, 1, stop);
+                    break;
+                }
+                run_item(item, warp, nwarps, stop0);
+            }
+        }
+    }
+    for (;;) {
+        int item = 0;
+        if (lane == 0) item = atomicAdd(P.item_counter, 1);
+        item = __shfl_sync(FULL, item, 0);
+        if (item >= items) break;
+        run_item(item, 0, 1, stop);
     }
 }
 

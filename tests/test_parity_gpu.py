@@ -848,3 +848,43 @@ def test_reverse_band_multistripe(aligner, kind):
     b = synth.from_pairs(pairs, sc)
     assert_parity(aligner.align(b), oracle_batch(b), b)
     assert aligner.batch_status()[0] == sw.SW_OK
+
+
+@pytest.mark.parametrize("kind", ["dna_mixed", "dna_cheap_gaps", "protein"])
+def test_reverse_cooperative_items(aligner, kind):
+    """Reverse items with >= SW_COOP_STRIPES stripes are swept by all warps of a CTA, consecutive
+    stripes on consecutive warps with published hand-off progress (sw_wavefront.cuh).  Long pairs
+    (8-20 stripes) of mixed identity -- unrelated pairs whose start lies far from the origin (cheap
+    gaps make their gapped score grow with length), high-identity ones, tandem repeats -- plus short
+    partners in the same items; all five fields vs the oracle."""
+    rng = np.random.default_rng({"dna_mixed": 41, "dna_cheap_gaps": 42, "protein": 43}[kind])
+    if kind == "protein":
+        alpha, sc, lo, hi = list("ARNDCQEGHILKMFPSTWYV"), synth.PROTEIN_SCORING, 1030, 1900
+    elif kind == "dna_cheap_gaps":
+        alpha, lo, hi = list("ACGT"), 1290, 2600
+        sc = {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -6, "gap_extend": -1}
+    else:
+        alpha, lo, hi = list("ACGT"), 1290, 3200
+        sc = {"alphabet": "dna", "match": 2, "mismatch": -3, "gap_open": -5, "gap_extend": -2}
+    pairs = []
+    for k in range(14):
+        n = int(rng.integers(lo, hi))
+        q = rng.choice(alpha, n)
+        u = k % 3
+        if u == 0:  # unrelated
+            r = rng.choice(alpha, int(rng.integers(n // 2, 2 * n)))
+        elif u == 1:  # related, embedded
+            r = q.copy()
+            mut = rng.random(n) < 0.05
+            r[mut] = rng.choice(alpha, int(mut.sum()))
+            r = np.concatenate([rng.choice(alpha, int(rng.integers(0, 500))), r, rng.choice(alpha, int(rng.integers(0, 500)))])
+        else:  # repeats
+            unit = rng.choice(alpha, int(rng.integers(2, 9)))
+            q = np.resize(unit, n)
+            r = np.resize(unit, n + int(rng.integers(-100, 300)))
+        pairs.append(("".join(q), "".join(r)))
+        pairs.append(("".join(rng.choice(alpha, int(rng.integers(100, 600)))), "".join(rng.choice(alpha, int(rng.integers(100, 900))))))
+    b = synth.from_pairs(pairs, sc)
+    for _ in range(2):
+        assert_parity(aligner.align(b), oracle_batch(b), b)
+        assert aligner.batch_status()[0] == sw.SW_OK
