@@ -37,7 +37,10 @@ constexpr int W16 = SW_W16, K16 = SW_K16;
 #ifndef SW_KP
 #define SW_KP 8
 #endif
-constexpr int WP = 16, KP = SW_KP;
+#ifndef SW_WP
+#define SW_WP 16
+#endif
+constexpr int WP = SW_WP, KP = SW_KP;
 constexpr int W32 = 16, K32 = 10;
 constexpr int WARPS_PER_BLOCK = 4;
 using G16 = Geometry<W16, K16, TS16>;
@@ -511,7 +514,14 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         std::memset(&hs, 0, sizeof(hs));
         hs.max_n = h->res_n;
         hs.max_m = h->res_m;
-        for (int r = 0; r < N_ROUTES; ++r) hs.fwd_count[r] = (int32_t)n_pairs;
+        // routes a pair within the reservation can take (pack's rule): launch only those
+        const bool tag_ok = K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA;
+        const int64_t smax_all = (int64_t)sc.max_sigma * std::min(h->res_n, h->res_m);
+        const bool all_tag = s16_ok && tag_ok && (int64_t)sc.max_sigma * h->res_n <= TAG_MAX_SCORE;
+        const bool any_s32 = !s16_ok || smax_all > S16_MAX_SCORE;
+        hs.fwd_count[ROUTE_TAG] = (s16_ok && tag_ok) ? (int32_t)n_pairs : 0;
+        hs.fwd_count[ROUTE_S16] = (s16_ok && !all_tag) ? (int32_t)n_pairs : 0;
+        hs.fwd_count[ROUTE_S32] = any_s32 ? (int32_t)n_pairs : 0;
     } else {
         SW_CUDA(h, cudaMemcpyAsync(h->h_stats, stats, sizeof(BatchStats), cudaMemcpyDeviceToHost, s));
         SW_CUDA(h, cudaStreamSynchronize(s));
