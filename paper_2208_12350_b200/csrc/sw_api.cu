@@ -96,6 +96,7 @@ struct sw_context {
     DevBuf<unsigned long long> keys_fwd, keys_rev;
     // codes
     DevBuf<uint8_t> qcode, rcode, rrev;
+    DevBuf<uint32_t> rcode4;  // SW_CODE4 measurement variant only
     // misc.  Per-slot state: the host-buffer entry point runs consecutive chunks of one batch
     // on two streams (slot k & 1), so their small kernels and tails overlap; slot 0 is the
     // device entry point's.
@@ -192,6 +193,21 @@ void release(DevBuf<T>& b) {
     if (b.p) cudaFree(b.p);
     b.p = nullptr; b.cap = 0;
 }
+
+#if SW_CODE4
+// measurement variant: byte codes -> 4-bit codes, 8 per word (nibble k of word w = byte 8w + k)
+__global__ void nibble_kernel(const uint8_t* __restrict__ c, uint32_t* __restrict__ c4, size_t words) {
+    for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (size_t)gridDim.x * blockDim.x) {
+        const uint2 b = reinterpret_cast<const uint2*>(c)[w];
+        uint32_t v = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v |= ((b.x >> (8 * k)) & 15u) << (4 * k);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v |= ((b.y >> (8 * k)) & 15u) << (16 + 4 * k);
+        c4[w] = v;
+    }
+}
+#endif
 
 // SW_MODE_POISON helper: p[0 .. n) = v.
 __global__ void fill_u32_kernel(uint32_t* p, size_t n, uint32_t v) {
@@ -589,7 +605,16 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     // 6. forward wavefront
     if (!spec_bin) SW_CUDA(h, cudaMemsetAsync(counters, 0, 8 * sizeof(int32_t), s));
     WaveParams W;
+#if SW_CODE4
+    if (!protein) {
+        const size_t words = h->rcode.cap / 8;
+        ENS(rcode4, words + 4);
+        nibble_kernel<<<(int)std::min<size_t>((words + 255) / 256, (size_t)h->sm_count * 8), 256, 0, s>>>(h->rcode.p, h->rcode4.p, words);
+        SW_CUDA(h, cudaGetLastError());
+    }
+#endif
     W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch[slot].p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
+    W.rcode4 = h->rcode4.p; W.sixteen = 16;
     W.progress = h->progress[slot].p;
     W.tag_mul = 64;
     W.one = 1;

@@ -48,6 +48,9 @@
 
 #define SV_QSTRIDE 512u  // bytes between quads of a saved column (32 lanes x 16 B), see Geometry::SVH
 #define U_MAX_FILL 8     // >= the column unroll x loop-body blocks + the prefetch distance: the hand-off fill margin
+#ifndef SW_CODE4
+#define SW_CODE4 0         // 1 (measurement variant): DNA TAG forward reads 4-bit reference codes, 8 per word
+#endif
 #ifndef SW_COOP_STRIPES
 #define SW_COOP_STRIPES 8  // reverse items with at least this many stripes are swept by all warps of a CTA
 #endif
@@ -144,6 +147,8 @@ struct WaveParams {
     uint32_t one;               // = 1; a kernel parameter so H = Hb + o is an IMAD (FMA pipe), not an IADD3
     Scoring sc;
     const BatchStats* stats;    // whole-batch failure flags (batch_rejected)
+    const uint32_t* rcode4;     // SW_CODE4 variant: the reference codes as nibbles (8 per word)
+    uint32_t sixteen;           // = 16 (opaque: IMAD.HI extraction stays on the FMA pipe)
 };
 
 template <int W, int K, class T>
@@ -475,6 +480,21 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     // NB blocks of U columns per loop iteration (the longer body lets ptxas keep loop-carried
     // values in place); tag bookkeeping stays per U-column block
     constexpr int NB = REV ? SW_REV_BODY_BLOCKS : SW_BODY_BLOCKS;
+    // SW_CODE4 (measurement variant, DNA TAG forward): the block's four codes per half come from two
+    // words of 4-bit codes prefetched one block ahead and one funnel shift; a code is extracted on the
+    // FMA pipe (shift left by IMAD, high word of a multiply by 16)
+    constexpr bool C4 = SW_CODE4 && TAG && !REV && NH == 2 && U == 4;
+    int64_t x4[NH];
+    uint32_t wa[NH], wb[NH], v4[NH];
+    if (C4) {
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            x4[h] = h_rpos[h] - L + c_lo;
+            wa[h] = __ldg(P.rcode4 + (x4[h] >> 3));
+            wb[h] = __ldg(P.rcode4 + (x4[h] >> 3) + 1);
+        }
+    }
+    const uint32_t sixteen = C4 ? P.sixteen : 16u;
     int t00 = 0;
     for (; t00 < T_end; t00 += U * NB) {
       wait_cols(c_lo + t00 + U * NB + U);
@@ -482,6 +502,16 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
       for (int bb = 0; bb < NB; ++bb) {
         const int t0 = t00 + bb * U;
         uint32_t nbt = REV ? 0u : best;  // TAG: running max of this block
+        if (C4) {
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                const int64_t x0 = x4[h] + t0;
+                v4[h] = __funnelshift_r(wa[h], wb[h], (uint32_t)(x0 & 7) * 4u);
+                const int64_t x1 = x0 + U;
+                wa[h] = __ldg(P.rcode4 + (x1 >> 3));
+                wb[h] = __ldg(P.rcode4 + (x1 >> 3) + 1);
+            }
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int t = t0 + u;
@@ -489,7 +519,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             uint32_t pw[NH][G::PWORDS];
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
-                const uint32_t src = prof_h[h] + cd[u % CD][h] * cs;
+                const uint32_t code = C4 ? __umulhi(v4[h] << (28 - 4 * u), sixteen) : cd[u % CD][h];
+                const uint32_t src = prof_h[h] + code * cs;
                 if (G::PWORDS >= 4) {
 #pragma unroll
                     for (int q4 = 0; q4 < G::PWORDS / 4; ++q4) {
@@ -502,7 +533,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     pw[h][0] = v.x;
                     if (G::PWORDS > 1) pw[h][G::PWORDS - 1] = v.y;
                 }
-                cd[u % CD][h] = ld_code(rp[h] + t + CD);
+                if (!C4) cd[u % CD][h] = ld_code(rp[h] + t + CD);
             }
             uint32_t bHO = b0, bF = 0u;
             if (MULTI) {
