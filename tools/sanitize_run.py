@@ -54,6 +54,15 @@ def main():
         pairs.append((q, "".join(rng.choice(list("ACGT"), int(rng.integers(0, 300)))) + q[: n - 7]))
     b = synth.from_pairs(pairs, {"alphabet": "dna", "match": 1, "mismatch": -1, "gap_open": -3, "gap_extend": -1})
     check("multi-stripe", a.align(b), b)
+    # CTA-cooperative reverse items (>= 8 stripes): long related / unrelated pairs
+    pairs = []
+    for k in range(6):
+        n = int(rng.integers(1300, 2000))
+        q = "".join(rng.choice(list("ACGT"), n))
+        r = q[: n - 11] if k % 2 == 0 else "".join(rng.choice(list("ACGT"), n + 300))
+        pairs.append((q, r))
+    b = synth.from_pairs(pairs, synth.DNA_SCORING)
+    check("cooperative reverse", a.align(b), b)
     # tie-heavy low-entropy DNA, several scorings (TAG / S16 / S32 routes)
     for sc in ({"alphabet": "dna", "match": 1, "mismatch": 0, "gap_open": -1, "gap_extend": -1},
                {"alphabet": "dna", "match": 2, "mismatch": -1, "gap_open": -3, "gap_extend": -1},
