@@ -170,7 +170,9 @@ def run_reference(args, rank: int):
     from paper_2208_12350_b200 import synth
     if rank != 0:
         return
-    b = synth.generate("c2", 0, 20_000)
+    key = args.workload
+    cfg = synth.CONFIGS[key]
+    b = synth.generate(key, 0, 20_000)
     import oracle
     cores = os.cpu_count() or 1
     # each step = a bounded prefix sample sized to ~6 s of oracle work
@@ -194,11 +196,12 @@ def run_reference(args, rank: int):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GCUPS", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": "c2_dna_100k_150x1024 (BASELINE configs[1]) -- bounded prefix sample per step",
-                   "pairs_per_step": sub.n_pairs, "cells_per_step": cells, "scoring": "3/-3/-6/-1"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle",
-                         "sample": f"first {sub.n_pairs} pairs of c2 ({cells:.3e} forward cells), forward+reverse"},
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name} (BASELINE configs[{cfg.index - 1}]: {cfg.baseline_text}) -- bounded prefix "
+                               f"sample per step", "pairs_per_step": sub.n_pairs, "cells_per_step": cells,
+                   "scoring": "DNA 3/-3/-6/-1", "batch_sha256": synth.batch_sha256(sub)},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GCUPS", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": f"first {sub.n_pairs} pairs of {key} ({cells:.3e} forward cells), forward+reverse"},
         "e2e": {"value": round(value, 4), "unit": "GCUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

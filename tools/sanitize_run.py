@@ -80,7 +80,7 @@ def main():
     out, _ = a.align_tensors(q, qo, r, ro, b.scoring)
     import torch
     torch.cuda.synchronize()
-    o = out[:, :b.n_pairs].cpu().numpy()
+    o = out[:3, :b.n_pairs].cpu().numpy()  # END_ONLY writes score / q_end / r_end only (the start rows stay unwritten)
     exp = oracle.align_batch(b.queries, b.q_offsets, b.refs, b.r_offsets, b.scoring)
     for i, f in enumerate(FIELDS[:3]):
         assert np.array_equal(o[i], exp[f]), f
