@@ -104,10 +104,14 @@ typedef struct {
  * (0x7f / 0xff), so any value a call reads or returns without having written
  * it in that call shows up as a wrong result instead of a stale plausible
  * one; results are unchanged, calls are slower.  Applies to every later call
- * on the handle.  Errors: SW_ERR_INVALID_ARGUMENT for an unknown mode bit.
+ * on the handle.  Flag SW_MODE_NO_BAND keeps every reverse-pass pair on the
+ * row-sweep kernels instead of the banded reverse kernels (DNA pairs whose
+ * score-S paths fit 32 / 64 diagonals; identical results --
+ * comparison and testing).  Errors: SW_ERR_INVALID_ARGUMENT for an unknown
+ * mode bit.
  */
 typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2, SW_MODE_TB_INT32 = 4,
-               SW_MODE_POISON = 8 } sw_mode_t;
+               SW_MODE_POISON = 8, SW_MODE_NO_BAND = 16 } sw_mode_t;
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
 
 /*

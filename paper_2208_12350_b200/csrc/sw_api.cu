@@ -17,6 +17,7 @@
 #include "sw_pack.cuh"
 #include "sw_wavefront.cuh"
 #include "sw_finish.cuh"
+#include "sw_band.cuh"
 #include "sw_traceback.cuh"
 
 using namespace swb;
@@ -96,6 +97,7 @@ struct sw_context {
     DevBuf<unsigned long long> keys_fwd, keys_rev;
     // codes
     DevBuf<uint8_t> qcode, rcode, rrev;
+    DevBuf<uint8_t> bslots;   // banded reverse pass (sw_band.cuh): slot 0 pads, pair p's slot p + 1
     DevBuf<uint32_t> rcode4;  // SW_CODE4 measurement variant only
     // misc.  Per-slot state: the host-buffer entry point runs consecutive chunks of one batch
     // on two streams (slot k & 1), so their small kernels and tails overlap; slot 0 is the
@@ -160,6 +162,17 @@ sw_status_t cuda_fail(sw_context* h, cudaError_t e, const char* what) {
     if (h) h->err = m;
     return e == cudaErrorMemoryAllocation ? SW_ERR_OUT_OF_MEMORY : SW_ERR_CUDA;
 }
+
+#ifndef SW_DEBUG_SYNC
+#define SW_DEBUG_SYNC 0  // development builds: synchronise after every launch of a call and name the failing one
+#endif
+#define SW_DBG(h, s, what)                                                                        \
+    do {                                                                                          \
+        if (SW_DEBUG_SYNC) {                                                                      \
+            cudaError_t _e = cudaStreamSynchronize(s);                                            \
+            if (_e != cudaSuccess) { fprintf(stderr, "sw debug: %s failed: %s\n", what, cudaGetErrorString(_e)); return cuda_fail((h), _e, what); } \
+        }                                                                                         \
+    } while (0)
 
 #define SW_CUDA(h, call)                                          \
     do {                                                          \
@@ -345,6 +358,14 @@ sw_status_t prepare_workspace(sw_context* h, size_t N, size_t tq, size_t tr, int
         SW_CUDA(h, cudaMemsetAsync(h->rrev.p, 0, h->rrev.cap, s));
         h->codes_alphabet = alphabet;
     }
+    // banded reverse pass (sw_band.cuh): slot 0 = pads (query pad codes, reference pad selectors: the empty
+    // halves of a work item read them), pair p's reversed prefixes in slot p + 1
+    uint8_t* old_b = h->bslots.p;
+    ENS(bslots, (N + 1) * BAND_SLOT);
+    if (h->bslots.p != old_b) {
+        SW_CUDA(h, cudaMemsetAsync(h->bslots.p, 0x04, h->bslots.cap, s));
+        SW_CUDA(h, cudaMemsetAsync(h->bslots.p + QREV_STRIDE, SEL_PAD, BAND_SLOT - QREV_STRIDE, s));
+    }
 #undef ENS
     return SW_OK;
 }
@@ -504,6 +525,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         pack_kernel<<<blocks, PACK_WARPS * 32, 0, s>>>(P);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
+        SW_DBG(h, s, "launch at sw_api.cu:527");
     }
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[1], s));
     // forward binning enqueued before the read-back below, assuming the common small-region
@@ -620,6 +642,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     W.one = 1;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p + lo;
     W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &stats->swept_fwd; W.counts = stats->fwd_count;
+    W.pre = nullptr;
     W.stats = stats;
     for (int r = 0; r < N_ROUTES; ++r) {
         if (lf[r].blocks <= 0) continue;
@@ -628,6 +651,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         void* args[] = {&W};
         SW_CUDA(h, cudaLaunchKernel(kfwd[r], dim3(lf[r].blocks), dim3(lf[r].warps * 32), args, (size_t)lf[r].smem, s));
         ++h->own_launches;
+        SW_DBG(h, s, "launch at sw_api.cu:652");
     }
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[4], s));
 
@@ -637,13 +661,17 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     F.rcode = h->rcode.p; F.rrev = h->rrev.p;
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
     F.target = h->target.p; F.key_rev = h->key.p; F.hist = hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
-    F.max_sigma = sc.max_sigma; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
+    F.max_sigma = sc.max_sigma; F.gap_open = sc.gap_open; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
+    const bool band_ok = !protein && s16_ok && K16 <= 16 && !(h->mode & SW_MODE_NO_BAND);
+    F.band_ok = band_ok ? 1 : 0; F.qcode = h->qcode.p; F.bslots = h->bslots.p;
+    F.rrev_bytes = (int64_t)h->rrev.cap; F.band_bytes = (int64_t)h->bslots.cap;
     F.out = *out; F.stats = stats; F.end_only = end_only ? 1 : 0; F.rev_small = small_rev ? 1 : 0;
     {
         const int64_t warps = std::min<int64_t>((hi - lo + FIN_PPW - 1) / FIN_PPW, (int64_t)h->sm_count * 64);
         finish_fwd_kernel<<<(int)((warps * 32 + 255) / 256), 256, 0, s>>>(F);
         SW_CUDA(h, cudaGetLastError());
         ++h->own_launches;
+        SW_DBG(h, s, "launch at sw_api.cu:671");
     }
     if (end_only) {  // forward pass only (sw_set_mode)
         if (timing) {
@@ -661,6 +689,25 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         SW_CUDA(h, cudaMemsetAsync(h->progress[slot].p, 0, h->progress[slot].cap * sizeof(unsigned long long), s));
     W.rcode = h->rrev.p; W.nlen = h->nlen_rev.p; W.mlen = h->mlen_rev.p; W.order = h->order_rev.p + lo;
     W.target = h->target.p; W.keys = h->keys_rev.p; W.swept = &stats->swept_rev; W.counts = stats->rev_count;
+    W.pre = stats->rev_band;  // the band pairs lead the reverse order
+    if (band_ok && hs.fwd_count[ROUTE_TAG] > 0) {
+        BandParams B;
+        B.slots = h->bslots.p; B.nlen = h->nlen_rev.p;
+        B.mlen = h->mlen_rev.p; B.target = h->target.p; B.order = h->order_rev.p + lo; B.band_counts = stats->rev_band;
+        B.keys = h->keys_rev.p; B.swept = &stats->swept_rev; B.sc = sc; B.stats = stats; B.tag_mul = 64;
+        const void* kb[N_BAND] = {(const void*)band_rev_kernel<2>, (const void*)band_rev_kernel<4>};
+        for (int b = 0; b < N_BAND; ++b) {
+            const int slots = 64 / band_lanes(b);
+            const int64_t items = (hs.fwd_count[ROUTE_TAG] + slots - 1) / slots;
+            const int64_t maxb = (int64_t)h->sm_count * occupancy_blocks(kb[b], 128, 0);
+            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((items + 3) / 4, maxb));
+            B.item_counter = counters + (b == 0 ? 3 : 7);
+            void* args[] = {&B};
+            SW_CUDA(h, cudaLaunchKernel(kb[b], dim3(blocks), dim3(128), args, 0, s));
+            ++h->own_launches;
+            SW_DBG(h, s, "launch at sw_api.cu:705");
+        }
+    }
     for (int r = 0; r < N_ROUTES; ++r) {
         if (lr[r].blocks <= 0) continue;
         W.route = r;
@@ -668,6 +715,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         void* args[] = {&W};
         SW_CUDA(h, cudaLaunchKernel(krev[r], dim3(lr[r].blocks), dim3(lr[r].warps * 32), args, (size_t)lr[r].smem, s));
         ++h->own_launches;
+        SW_DBG(h, s, "launch at sw_api.cu:714");
     }
     if (timing) SW_CUDA(h, cudaEventRecord(h->ev[6], s));
 
@@ -675,6 +723,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     finish_rev_kernel<<<(int)std::min<int64_t>((hi - lo + 255) / 256, (int64_t)h->sm_count * 16), 256, 0, s>>>(F);
     SW_CUDA(h, cudaGetLastError());
     ++h->own_launches;
+    SW_DBG(h, s, "launch at sw_api.cu:721");
     if (timing) {
         SW_CUDA(h, cudaEventRecord(h->ev[7], s));
         h->ev_valid = true;
@@ -1049,7 +1098,7 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
 
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
-    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32 | SW_MODE_POISON))
+    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32 | SW_MODE_POISON | SW_MODE_NO_BAND))
         return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
     h->mode = mode;
     return SW_OK;
@@ -1184,7 +1233,7 @@ sw_status_t sw_free(sw_handle_t h) {
     release(h->iota); release(h->order); release(h->order_rev); release(h->qpos); release(h->rpos); release(h->flags);
     release(h->key); release(h->key_sorted);
     for (int k = 0; k < N_SLOTS; ++k) { release(h->cub_temp[k]); release(h->scratch[k]); release(h->progress[k]); } release(h->keys_fwd); release(h->keys_rev);
-    release(h->qcode); release(h->rcode); release(h->rrev);
+    release(h->qcode); release(h->rcode); release(h->rrev); release(h->bslots);
     release(h->st_q); release(h->st_r); release(h->st_qo); release(h->st_ro); release(h->st_out);
     release(h->db_q); release(h->db_qo);
     if (h->d_stats) cudaFree(h->d_stats);

@@ -82,6 +82,25 @@ struct Scoring {
     int max_sigma; // largest s(a,b)
 };
 
+// Gap-aware diagonal band of the reverse pass (reading R6).  Every score-S
+// path of the reversed rectangle (n2 x m2) starts at its origin with an aligned pair; a cell of it on
+// diagonal d = j' - i' > 0 needs >= d deletion columns, d < 0 needs >= -d insertion rows (each of
+// which also forgoes its aligned pair), and any gap run costs |o| + (k-1)|e|.  With M <= n2 - I and
+// M <= m2 - D aligned pairs scoring <= ms each:
+//   -DI <= d <= DD,  DI = (ms n2 - S - (|o| - |e|)) / (ms + |e|),
+//   DD = min((ms n2 - S - (|o| - |e|)) / |e|, (ms m2 - S - (|o| - |e|)) / (ms + |e|)).
+// (go = -gap_open, ge = -gap_extend; clamped at 0: no gap fits -> the path is one diagonal.)
+__host__ __device__ inline void rev_band(int ms, int go, int ge, int S, int n2, int m2, int& DI, int& DD) {
+    const long long g0 = (long long)go - ge;
+    long long slack = (long long)ms * n2 - S - g0, slack_m = (long long)ms * m2 - S - g0;
+    slack = slack < 0 ? 0 : slack;
+    slack_m = slack_m < 0 ? 0 : slack_m;
+    long long di = slack / (ms + ge), dd = slack_m / (ms + ge);
+    if (ge > 0 && slack / ge < dd) dd = slack / ge;
+    DI = (int)(di < 0x3fffffffLL ? di : 0x3fffffffLL);
+    DD = (int)(dd < 0x3fffffffLL ? dd : 0x3fffffffLL);
+}
+
 __device__ __forceinline__ int sigma_of(const Scoring& sc, int a, int b) {
     if (sc.alphabet == SW_ALPHABET_DNA) return a == b ? sc.match : sc.mismatch;
     return c_blosum62[a][b];

@@ -5,6 +5,7 @@
 #include "sw_common.cuh"
 #include "sw_pack.cuh"
 #include "sw_bin.cuh"
+#include "sw_band.cuh"
 
 namespace swb {
 
@@ -23,7 +24,11 @@ struct FinishParams {
     uint32_t* key_rev;              // reverse work key per pair (0: no reverse work)
     uint32_t* hist;                 // bin histogram (zero on entry)
     int rows_s16, rows_s32;
-    int max_sigma, gap_extend;
+    int max_sigma, gap_open, gap_extend;
+    int band_ok;                    // DNA TAG batches: narrow-band pairs take the banded reverse kernels (sw_band.cuh)
+    const uint8_t* qcode;           // query codes (band pairs' reversed query prefixes)
+    uint8_t* bslots;                // band buffer (sw_band.cuh): pair p's slot at (p + 1) * BAND_SLOT
+    int64_t rrev_bytes, band_bytes; // buffer sizes (SW_BAND_CHECK builds)
     uint8_t pad_code;
     int end_only;                   // forward pass only: no start outputs, no reverse-pass preparation
     int rev_small;                  // the reverse pass is counting-sorted on exact (stripes, columns) bins
@@ -56,6 +61,7 @@ constexpr int FIN_FB = SW_FIN_FB;   // words per lane loaded before any is store
 
 __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     __shared__ int s_route[N_ROUTES];
+    __shared__ int s_band[N_BAND];
     if (batch_rejected(P.stats)) {  // whole batch invalid (malformed / beyond the reservation): every field -1
         for (int64_t p = P.lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P.hi; p += (int64_t)gridDim.x * blockDim.x) {
             P.out.score[p] = -1; P.out.q_end[p] = -1; P.out.r_end[p] = -1;
@@ -64,18 +70,21 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
         return;
     }
     if (threadIdx.x < N_ROUTES) s_route[threadIdx.x] = 0;
+    if (threadIdx.x < N_BAND) s_band[threadIdx.x] = 0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     int l_route[N_ROUTES] = {0, 0, 0};
+    int l_band[N_BAND] = {0, 0};
     const uint32_t padw = (uint32_t)P.pad_code * 0x01010101u;
     const uint32_t* src = reinterpret_cast<const uint32_t*>(P.rcode);
     uint32_t* dst = reinterpret_cast<uint32_t*>(P.rrev);
+    uint32_t* bdst = reinterpret_cast<uint32_t*>(P.bslots);
     for (int64_t base = P.lo + gw * FIN_PPW; base < P.hi; base += nw * FIN_PPW) {
         const int64_t p = base + lane;
-        int64_t rp = 0, w0 = 0;
-        int j = -1, cnt = 0;
+        int64_t rp = 0, w0 = 0, kb = 0, soff = 0;  // k = a - kb (reversed index), source = soff - a
+        int j = -1, cnt = 0, form = 0, band = -1, n2b = 0;
         if (lane < FIN_PPW && p < P.hi) {
             P.keys_rev[p] = 0ull;
             const uint8_t fl = P.flags[p];
@@ -95,6 +104,7 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
             } else {
                 P.out.score[p] = S; P.out.q_end[p] = i; P.out.r_end[p] = j;
                 const int n2 = i + 1;
+                n2b = n2;
                 // Columns the reverse pass can need (reading R6): every score-S alignment in the
                 // reversed rectangle starts at its origin (SURVEY.md 8(c) C-5 proof) and spans
                 // M + I columns, M <= n2 aligned pairs and I gap columns each costing >= |e|, so
@@ -107,6 +117,15 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                 int route = flag_route(fl);
                 // TAG reverse items need H <= 511 in every swept cell, also past the rectangle
                 if (route == ROUTE_TAG && (long long)P.max_sigma * n2 > TAG_MAX_SCORE) route = ROUTE_S16;
+                // banded reverse pass (sw_band.cuh) when the pair's score-S paths fit 32 / 64 diagonals
+                // and its rrev region has room for the selectors the kernel reads
+                if (route == ROUTE_TAG && P.band_ok && n2 <= BAND_MAX_N2) {
+                    int DI, DD;
+                    rev_band(P.max_sigma, -P.gap_open, -P.gap_extend, S, n2, m2, DI, DD);
+                    const int need = -band_dlo(DI) + DD + 1;
+                    for (int b = 0; b < N_BAND && band < 0; ++b)
+                        if (DI <= 32 && need <= band_cap(b)) band = b;
+                }
                 const int rows = route == ROUTE_S32 ? P.rows_s32 : P.rows_s16;
                 const uint32_t stripes = (uint32_t)((n2 + rows - 1) / rows);
                 P.nlen_rev[p] = n2;
@@ -122,19 +141,39 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                 // cells-rows), then columns: an unrelated long pair whose gapped score grows with its
                 // length (no narrow band) can outweigh a higher-identity pair with more stripes
                 const int B = (S + P.max_sigma - 1) / P.max_sigma;
-                const int band = max(1, (int)min((long long)m2, (long long)n2 + m2 - 2LL * B + rows));
+                const int bcols = max(1, (int)min((long long)m2, (long long)n2 + m2 - 2LL * B + rows));
                 const uint32_t key = stripes == 1 ? work_key(route, 1u, (uint32_t)S)
-                                   : P.rev_small ? work_key(route, stripes, (uint32_t)band)
-                                   : work_key(route, (uint32_t)min(0x3fffLL, ((long long)stripes * band) >> 8) + 1u, (uint32_t)band);
-                P.key_rev[p] = key;
-                const uint32_t bin = key_bin(key);
-                if (bin) atomicAdd(P.hist + bin, 1u);
-                ++l_route[route];
-                // output words covering rrev[rp - PADL .. rp + j + REV_PAD]: PADL pad codes (the
-                // reverse sweep's fill columns), the reversed prefix, then REV_PAD pad codes
+                                   : P.rev_small ? work_key(route, stripes, (uint32_t)bcols)
+                                   : work_key(route, (uint32_t)min(0x3fffLL, ((long long)stripes * bcols) >> 8) + 1u, (uint32_t)bcols);
                 rp = P.rpos[p];
-                w0 = (rp - PADL) >> 2;
-                cnt = (int)(((rp + j + REV_PAD) >> 2) - w0 + 1);
+                if (band >= 0) {
+                    // band pairs first in the reverse order (TAG rank, stripe fields above any TAG
+                    // pair's), grouped by n2; their own counts (BatchStats::rev_band)
+                    const uint32_t bkey = work_key(ROUTE_TAG, P.rev_small ? (uint32_t)(BIN_MAX_STRIPES - band) : 0x3fffu - band,
+                                                   (uint32_t)n2);
+                    P.key_rev[p] = bkey;
+                    const uint32_t bin = key_bin(bkey);
+                    if (bin) atomicAdd(P.hist + bin, 1u);
+                    ++l_band[band];
+                    // output words covering the slot's selectors j' in [-32, JW): the reversed prefix as
+                    // A-form PRMT selectors, pad selectors around it (sw_band.cuh)
+                    kb = (p + 1) * BAND_SLOT + BAND_ROFF;
+                    w0 = (kb - 32) >> 2;
+                    cnt = (32 + band_jw(n2, band_cap(band))) >> 2;
+                    soff = rp + kb + j;
+                    form = 1;
+                } else {
+                    P.key_rev[p] = key;
+                    const uint32_t bin = key_bin(key);
+                    if (bin) atomicAdd(P.hist + bin, 1u);
+                    ++l_route[route];
+                    // output words covering rrev[rp - PADL .. rp + j + REV_PAD]: PADL pad codes (the
+                    // reverse sweep's fill columns), the reversed prefix, then REV_PAD pad codes
+                    kb = rp;
+                    w0 = (rp - PADL) >> 2;
+                    cnt = (int)(((rp + j + REV_PAD) >> 2) - w0 + 1);
+                    soff = 2 * rp + j;
+                }
             }
         }
         // flat list of the warp's words: inclusive scan of the per-pair word counts
@@ -149,7 +188,7 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
         for (int g0 = 0; g0 < total; g0 += 32 * FIN_FB) {
             uint32_t x0[FIN_FB], x1[FIN_FB], sel[FIN_FB];
             int64_t aa[FIN_FB], kk0[FIN_FB];
-            int jj[FIN_FB];
+            int jj[FIN_FB], ff[FIN_FB];
 #pragma unroll
             for (int u = 0; u < FIN_FB; ++u) {
                 const int g = g0 + u * 32 + lane;
@@ -160,18 +199,20 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                     const int e = __shfl_sync(FULL, excl, own + st);
                     if (e <= g) own += st;
                 }
-                const int64_t orp = __shfl_sync(FULL, rp, own);
+                const int64_t okb = __shfl_sync(FULL, kb, own);
+                const int64_t osoff = __shfl_sync(FULL, soff, own);
                 const int64_t ow0 = __shfl_sync(FULL, w0, own);
                 const int oj = __shfl_sync(FULL, j, own);
                 const int oex = __shfl_sync(FULL, excl, own);
+                const int oform = __shfl_sync(FULL, form, own);
                 const int64_t a = (ow0 + (g - oex)) * 4;  // rrev index of the word's byte 0
-                // byte b of the word is rrev[a + b] = rcode[2 rp + j - a - b] (k = a + b - rp)
-                const int64_t sbeg = 2 * orp + oj - a - 3;  // lowest source index (byte 3)
+                // byte b of the word is rrev[a + b] = rcode[soff - a - b] (k = a + b - kb)
+                const int64_t sbeg = osoff - a - 3;  // lowest source index (byte 3)
                 const uint32_t o = (uint32_t)(sbeg & 3);
-                aa[u] = a; kk0[u] = a - orp; jj[u] = oj;
+                aa[u] = a; kk0[u] = a - okb; jj[u] = oj; ff[u] = oform;
                 sel[u] = (o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12);
                 x0[u] = 0; x1[u] = 0;
-                if (g < total) {
+                if (g < total && sbeg >= 0) {  // (a band word past the prefix can point before the buffer: all pads)
                     x0[u] = __ldg(src + (sbeg >> 2));
                     x1[u] = __ldg(src + (sbeg >> 2) + 1);
                 }
@@ -186,15 +227,67 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                     for (int b = 0; b < 4; ++b)
                         if (k0 + b < 0 || k0 + b > jj[u]) v = (v & ~(0xffu << (8 * b))) | (padw & (0xffu << (8 * b)));
                 }
-                dst[aa[u] >> 2] = v;
+                if (ff[u]) {
+                    // A-form selectors (sw_band.cuh): code c < 4 -> c * 0x11 + 0x80, pad (4) -> SEL_PAD 0x88
+                    const uint32_t pads = (v >> 2) & 0x01010101u;
+                    v = v * 0x11u + 0x80808080u - pads * 0x3cu;
+                }
+#if SW_BAND_CHECK
+                if (aa[u] < 0 || aa[u] + 4 > (ff[u] ? P.band_bytes : P.rrev_bytes)) { printf("finish write out of buffer %lld\n", (long long)aa[u]); __trap(); }
+#endif
+                (ff[u] ? bdst : dst)[aa[u] >> 2] = v;
+            }
+        }
+        // band pairs' reversed query prefixes: the pair's whole QREV_STRIDE slot, q'[i] = q[n2 - 1 - i] at
+        // QREV_PAD + i, pad codes elsewhere; two words per lane, each one PRMT of two aligned source words
+        unsigned bmask = __ballot_sync(FULL, lane < FIN_PPW && band >= 0);
+        while (bmask) {
+            const int src_l = __ffs(bmask) - 1;
+            bmask &= bmask - 1;
+            const int64_t bp = base + src_l;
+            const int bn2 = __shfl_sync(FULL, n2b, src_l);
+            const int64_t qp = P.qpos[bp];
+            const uint32_t* qs = reinterpret_cast<const uint32_t*>(P.qcode);
+            uint32_t* qd = reinterpret_cast<uint32_t*>(P.bslots + (bp + 1) * BAND_SLOT);
+#pragma unroll
+            for (int w = 0; w < 2; ++w) {
+                const int x = (2 * lane + w) * 4;       // slot byte of the word's byte 0
+                const int i0 = x - QREV_PAD;            // q' index of byte 0
+                // byte b = q'[i0 + b] = qcode[qp + bn2 - 1 - i0 - b]
+                const int64_t sbeg = qp + bn2 - 1 - i0 - 3;
+                uint32_t v = 0x04040404u;
+                if (i0 + 3 >= 0 && i0 < bn2) {
+                    const int64_t sb = sbeg > 0 ? sbeg : 0;   // words entirely outside are never loaded
+                    const uint32_t o = (uint32_t)(sb & 3);
+                    const uint32_t y0 = __ldg(qs + (sb >> 2)), y1 = __ldg(qs + (sb >> 2) + 1);
+                    v = __byte_perm(y0, y1, (o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
+                    if (sbeg < 0 || i0 < 0 || i0 + 3 >= bn2) {
+                        uint32_t m = 0;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int ib = i0 + b;
+                            const uint32_t cb = (ib >= 0 && ib < bn2) ? (uint32_t)P.qcode[qp + bn2 - 1 - ib] : 4u;
+                            m |= cb << (8 * b);
+                        }
+                        v = m;
+                    }
+                }
+#if SW_BAND_CHECK
+                if ((bp + 2) * BAND_SLOT > P.band_bytes) { printf("finish qrev write out of buffer %lld\n", (long long)bp); __trap(); }
+#endif
+                qd[2 * lane + w] = v;
             }
         }
     }
-    if (lane < FIN_PPW)
+    if (lane < FIN_PPW) {
         for (int r = 0; r < N_ROUTES; ++r)
             if (l_route[r]) atomicAdd(&s_route[r], l_route[r]);
+        for (int b = 0; b < N_BAND; ++b)
+            if (l_band[b]) atomicAdd(&s_band[b], l_band[b]);
+    }
     __syncthreads();
     if (threadIdx.x < N_ROUTES && s_route[threadIdx.x]) atomicAdd(&P.stats->rev_count[threadIdx.x], s_route[threadIdx.x]);
+    if (threadIdx.x < N_BAND && s_band[threadIdx.x]) atomicAdd(&P.stats->rev_band[threadIdx.x], s_band[threadIdx.x]);
 }
 
 // After the reverse pass: q_start = q_end - i', r_start = r_end - j'.

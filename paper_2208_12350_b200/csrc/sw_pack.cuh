@@ -24,6 +24,7 @@ struct BatchStats {
     int32_t rejected;       // reserved (asynchronous) call: the batch exceeds the reservation (sw_reserve)
     int32_t fwd_count[4];   // valid, non-trivial pairs per route (forward pass)
     int32_t rev_count[4];   // pairs with S > 0 per route (reverse pass)
+    int32_t rev_band[2];    // of which on the banded reverse routes (32 / 64 diagonals, sw_band.cuh)
 };
 constexpr size_t STATS_PER_BATCH_OFFSET = offsetof(BatchStats, max_n);
 

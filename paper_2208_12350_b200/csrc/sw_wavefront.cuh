@@ -135,6 +135,7 @@ struct WaveParams {
     const int32_t* mlen;        // columns (forward: m, reverse: r_end+1)
     const int32_t* order;       // pair ids sorted by work key (routes in order TAG, S16, S32)
     const int32_t* counts;      // device: pairs per route for this pass
+    const int32_t* pre;         // reverse pass: pairs ahead of the routes in the order (the banded ones), else null
     int route;                  // this launch's route
     const int32_t* target;      // reverse: forward score per pair
     unsigned long long* keys;   // per-pair atomicMax output
@@ -520,6 +521,12 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
                 const uint32_t code = C4 ? __umulhi(v4[h] << (28 - 4 * u), sixteen) : cd[u % CD][h];
+#ifdef SW_BAND_CHECK
+                if (SW_BAND_CHECK && code >= (uint32_t)nc) {
+                    printf("wave code %u >= nc: REV %d route %d pid %d t %d L %d\n", code, (int)REV, P.route, h_pid[h], t, L);
+                    __trap();
+                }
+#endif
                 const uint32_t src = prof_h[h] + code * cs;
                 if (G::PWORDS >= 4) {
 #pragma unroll
@@ -972,7 +979,7 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
     const int n_path = P.counts[P.route];
-    int first = 0;
+    int first = P.pre ? P.pre[0] + P.pre[1] : 0;
     for (int r = 0; r < P.route; ++r) first += P.counts[r];
     const int items = (n_path + SLOTS - 1) / SLOTS;
     const uint32_t o2 = T::lift(P.sc.gap_open);  // H = Hb + o as one 32-bit add
@@ -1053,15 +1060,21 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
                 if (lane < SLOTS && s_pid >= 0) {
                     const int ms = P.sc.max_sigma;
                     const int B = (s_tgt + ms - 1) / ms;
+                    // gap-aware diagonal band (sw_common.cuh rev_band): rows [row0, r1] of a stripe
+                    // need columns [row0 - DI, r1 + DD] only
+                    int DI, DD;
+                    rev_band(ms, -P.sc.gap_open, -P.sc.gap_extend, s_tgt, s_n, s_m, DI, DD);
                     if (row0 >= s_n) {
                         s_lim = 0;  // no row of this half in the stripe
                     } else {
                         const int r1 = min(row0 + G::ROWS, s_n) - 1;
-                        lo = max(0, B - s_n + row0);
-                        s_lim = min(s_m, s_m + r1 - B + 1) + W - 1;
+                        lo = max(max(0, B - s_n + row0), row0 - DI);
+                        s_lim = min(min(s_m, s_m + r1 - B + 1), (int)min((int64_t)0x3fffffff, (int64_t)r1 + DD + 1)) + W - 1;
                     }
-                    if (row0 + G::ROWS < s_n)
-                        nl = min(s_m, s_m + min(row0 + 2 * G::ROWS, s_n) - B) + W - 1;
+                    if (row0 + G::ROWS < s_n) {
+                        const int r1n = min(row0 + 2 * G::ROWS, s_n) - 1;
+                        nl = min(min(s_m, s_m + r1n + 1 - B), (int)min((int64_t)0x3fffffff, (int64_t)r1n + DD + 1)) + W - 1;
+                    }
                 }
 #pragma unroll
                 for (int d = 16; d >= 1; d >>= 1) {

@@ -888,3 +888,111 @@ def test_reverse_cooperative_items(aligner, kind):
     for _ in range(2):
         assert_parity(aligner.align(b), oracle_batch(b), b)
         assert aligner.batch_status()[0] == sw.SW_OK
+
+
+@pytest.mark.parametrize("scoring", [(3, -3, -6, -1), (2, -3, -5, -2), (1, -1, -2, 0), (5, -4, -4, -4), (1, -4, -6, -3)])
+def test_reverse_gap_band_edges(aligner, scoring):
+    """Gap-aware reverse band (sw_wavefront.cuh): a score-S path from the reversed origin drifts at
+    most DD = (ms n2 - S - (|o| - |e|)) / |e| diagonals right and DI = (ms n2 - S - (|o| - |e|)) /
+    (ms + |e|) left.  Pairs whose optimal alignment carries one deletion / insertion run of length k
+    sit exactly on that edge (slack = k|e| resp. k(ms + |e|)); mixed with several runs, random
+    flanks, single- and multi-stripe lengths, zero-cost extension (e = 0) and linear gaps."""
+    ma, mm, o, e = scoring
+    sc = {"alphabet": "dna", "match": ma, "mismatch": mm, "gap_open": o, "gap_extend": e}
+    rng = np.random.default_rng(1000 + ma * 7 - mm * 3 - o - e)
+    A = list("ACGT")
+    pairs = []
+    for t in range(60):
+        n = int(rng.choice([40, 150, 170, 333, 700, 1500]))
+        x = rng.choice(A, n)
+        k = int(rng.integers(1, 40))
+        cut = int(rng.integers(1, n))
+        kind = t % 4
+        if kind == 0:    # deletion run of k reference residues
+            q = x
+            r = np.concatenate([x[:cut], rng.choice(A, k), x[cut:]])
+        elif kind == 1:  # insertion run of k query residues
+            q = np.concatenate([x[:cut], rng.choice(A, k), x[cut:]])
+            r = x
+        elif kind == 2:  # several runs of both kinds
+            q, r = list(x), list(x)
+            for _ in range(int(rng.integers(2, 5))):
+                c, kk = int(rng.integers(1, len(q))), int(rng.integers(1, 12))
+                if rng.random() < 0.5:
+                    r[c:c] = list(rng.choice(A, kk))
+                else:
+                    q[c:c] = list(rng.choice(A, kk))
+            q, r = np.array(q), np.array(r)
+        else:            # substitutions plus one run
+            q = x.copy()
+            mut = rng.random(n) < 0.02
+            q[mut] = rng.choice(A, int(mut.sum()))
+            r = np.concatenate([x[:cut], rng.choice(A, k), x[cut:]])
+        fl = [rng.choice(A, int(rng.integers(0, 200))), rng.choice(A, int(rng.integers(0, 200)))]
+        r = np.concatenate([fl[0], r, fl[1]])
+        pairs.append(("".join(q), "".join(r)))
+    b = synth.from_pairs(pairs, sc)
+    assert_parity(aligner.align(b), oracle_batch(b), b)
+    assert aligner.batch_status()[0] == sw.SW_OK
+
+
+@pytest.mark.parametrize("kind", ["c2", "c1_scorings", "repeats", "indels"])
+def test_banded_reverse_matches_row_sweep(kind):
+    """Banded reverse kernels (sw_band.cuh: lanes own diagonals of the score-S band) against the
+    oracle and against the row-sweep reverse pass (SW_MODE_NO_BAND) on the same batch: all five
+    fields; the banded pass sweeps far fewer reverse cells on ADEPT-shaped reads."""
+    import torch
+    assert torch.cuda.is_available()
+    rng = np.random.default_rng({"c2": 51, "c1_scorings": 52, "repeats": 53, "indels": 54}[kind])
+    batches = []
+    if kind == "c2":
+        batches.append(synth.generate("c2", 0, 6000))
+    elif kind == "c1_scorings":
+        base = synth.generate("c1")
+        for sc in [(3, -3, -6, -1), (2, -3, -5, -2), (1, -1, -2, 0), (5, -4, -4, -4), (2, -8, -3, -3), (4, 2, -9, -1)]:
+            s = {"alphabet": "dna", "match": sc[0], "mismatch": sc[1], "gap_open": sc[2], "gap_extend": sc[3]}
+            batches.append(synth.from_pairs([base.pair(p) for p in range(base.n_pairs)], s))
+    elif kind == "repeats":
+        pairs = []
+        for _ in range(600):
+            unit = "".join(rng.choice(list("ACGT"), int(rng.integers(1, 6))))
+            n = int(rng.integers(20, 176))
+            q = (unit * (n // len(unit) + 2))[:n]
+            r = "".join(rng.choice(list("ACGT"), int(rng.integers(0, 40)))) + (unit * 80)[: n + int(rng.integers(-10, 60))] + \
+                "".join(rng.choice(list("ACGT"), int(rng.integers(0, 40))))
+            pairs.append((q, r))
+        batches.append(synth.from_pairs(pairs, {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -6, "gap_extend": -1}))
+    else:
+        pairs = []
+        A = list("ACGT")
+        for t in range(800):
+            n = int(rng.integers(8, 176))
+            x = rng.choice(A, n)
+            q, r = list(x), list(x)
+            for _ in range(int(rng.integers(0, 4))):
+                c, kk = int(rng.integers(0, len(q) + 1)), int(rng.integers(1, 20))
+                if rng.random() < 0.5:
+                    r[c:c] = list(rng.choice(A, kk))
+                else:
+                    q[c:c] = list(rng.choice(A, kk))
+            q = q[:176]
+            fl = [rng.choice(A, int(rng.integers(0, 300))), rng.choice(A, int(rng.integers(0, 300)))]
+            pairs.append(("".join(q), "".join(fl[0]) + "".join(r) + "".join(fl[1])))
+        batches.append(synth.from_pairs(pairs, {"alphabet": "dna", "match": 2, "mismatch": -3, "gap_open": -5, "gap_extend": -2}))
+    a = sw.Aligner(0, poison=True)
+    try:
+        for b in batches:
+            exp = oracle_batch(b)
+            a.set_mode(sw.SW_MODE_NO_BAND)
+            got_rows = a.align(b)
+            rev_rows = a.reverse_cells()
+            a.set_mode(sw.SW_MODE_FULL)
+            got_band = a.align(b)
+            rev_band = a.reverse_cells()
+            assert_parity(got_rows, exp, b)
+            assert_parity(got_band, exp, b)
+            assert a.batch_status()[0] == sw.SW_OK
+            if kind == "c2":
+                assert rev_band < 0.6 * rev_rows, (rev_band, rev_rows)
+    finally:
+        a.close()
