@@ -45,6 +45,7 @@ constexpr int WP = SW_WP, KP = SW_KP;
 constexpr int W32 = 16, K32 = 10;
 constexpr int WARPS_PER_BLOCK = 4;
 using G16 = Geometry<W16, K16, TS16>;
+using G16F = Geometry<W16, K16, TS16, SW_IMERGE && SW_TAG_LAZY && K16 == 10>;  // DNA TAG forward kernels
 using GP = Geometry<WP, KP, TS16>;
 using G32 = Geometry<W32, K32, TS32>;
 
@@ -295,7 +296,7 @@ void plan_waves(const sw_context* h, const Scoring& sc, bool protein, const Batc
     for (int r = 0; r < N_ROUTES; ++r) {
         // reverse-pass pairs are a subset of the forward ones (finish_fwd may move TAG pairs to
         // S16): forward counts bound the grids
-        const bool demote = (int64_t)sc.max_sigma * hs.max_n > TAG_MAX_SCORE;  // finish_fwd's TAG -> S16 rule
+        const bool demote = protein || (int64_t)sc.max_sigma * hs.max_n > TAG_MAX_SCORE;  // finish_fwd's TAG -> S16 rule
         const int64_t rev_upper = hs.fwd_count[r] + (r == ROUTE_S16 && demote ? hs.fwd_count[ROUTE_TAG] : 0);
         if (r == ROUTE_S32) {
             lf[r] = plan_wave<G32>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
@@ -305,7 +306,8 @@ void plan_waves(const sw_context* h, const Scoring& sc, bool protein, const Batc
             lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], 3);
             lr[r] = plan_wave<GP>(h, krev[r], sc.nc, rev_upper, 3);
         } else {
-            lf[r] = plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
+            lf[r] = r == ROUTE_TAG ? plan_wave<G16F>(h, kfwd[r], sc.nc, hs.fwd_count[r])
+                                   : plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);
             lr[r] = plan_wave<G16>(h, krev[r], sc.nc, rev_upper);
         }
     }
@@ -511,7 +513,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         PackParams P;
         P.queries = queries; P.q_off = q_off; P.refs = refs; P.r_off = r_off; P.lo = lo; P.hi = hi;
         P.q0 = q0; P.qN = qN; P.r0 = r0; P.rN = rN; P.qshift = qshift; P.rshift = rshift;
-        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA) ? 1 : 0;  // TAG route: DNA batches
+        P.alphabet = sc.alphabet; P.s16_ok = s16_ok ? 1 : 0; P.max_sigma = sc.max_sigma; P.tag_ok = tag_max_score(sc.alphabet) > 0 && (K16 <= 16 || protein) ? 1 : 0;  // TAG route (DNA; protein: PT)
         P.rows_s16 = rows16; P.rows_s32 = rows32;
         P.ext_dev = spec ? 1 : 0; P.n_all = n_pairs;
         P.qcap = (int64_t)h->qcode.cap; P.rcap = (int64_t)std::min(h->rcode.cap, h->rrev.cap);
@@ -553,9 +555,9 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
         hs.max_n = h->res_n;
         hs.max_m = h->res_m;
         // routes a pair within the reservation can take (pack's rule): launch only those
-        const bool tag_ok = K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA;
+        const bool tag_ok = tag_max_score(sc.alphabet) > 0 && (K16 <= 16 || protein);
         const int64_t smax_all = (int64_t)sc.max_sigma * std::min(h->res_n, h->res_m);
-        const bool all_tag = s16_ok && tag_ok && (int64_t)sc.max_sigma * h->res_n <= TAG_MAX_SCORE;
+        const bool all_tag = s16_ok && tag_ok && (int64_t)sc.max_sigma * h->res_n <= tag_max_score(sc.alphabet);
         const bool any_s32 = !s16_ok || smax_all > S16_MAX_SCORE;
         hs.fwd_count[ROUTE_TAG] = (s16_ok && tag_ok) ? (int32_t)n_pairs : 0;
         hs.fwd_count[ROUTE_S16] = (s16_ok && !all_tag) ? (int32_t)n_pairs : 0;
@@ -638,7 +640,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     W.qpos = h->qpos.p; W.rpos = h->rpos.p; W.scratch = h->scratch[slot].p; W.scratch_seg_bytes = seg_bytes; W.sc = sc;
     W.rcode4 = h->rcode4.p; W.sixteen = 16;
     W.progress = h->progress[slot].p;
-    W.tag_mul = 64;
+    W.tag_mul = protein ? 8 : 64;  // DNA TAG: H * 64 + 6 tag bits; protein (PT): H * 8 + 3 row bits
     W.one = 1;
     W.qcode = h->qcode.p; W.rcode = h->rcode.p; W.nlen = h->nlen.p; W.mlen = h->mlen.p; W.order = h->order.p + lo;
     W.target = nullptr; W.keys = h->keys_fwd.p; W.swept = &stats->swept_fwd; W.counts = stats->fwd_count;
@@ -663,7 +665,7 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     F.target = h->target.p; F.key_rev = h->key.p; F.hist = hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
     F.max_sigma = sc.max_sigma; F.gap_open = sc.gap_open; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
     const bool band_ok = !protein && s16_ok && K16 <= 16 && !(h->mode & SW_MODE_NO_BAND);
-    F.band_ok = band_ok ? 1 : 0; F.qcode = h->qcode.p; F.bslots = h->bslots.p;
+    F.band_ok = band_ok ? 1 : 0; F.protein = protein ? 1 : 0; F.qcode = h->qcode.p; F.bslots = h->bslots.p;
     F.rrev_bytes = (int64_t)h->rrev.cap; F.band_bytes = (int64_t)h->bslots.cap;
     F.out = *out; F.stats = stats; F.end_only = end_only ? 1 : 0; F.rev_small = small_rev ? 1 : 0;
     {
@@ -947,7 +949,7 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
 #undef ENS
     // Chunks of about equal cell count; chunk k+1's host-to-device copy (copy stream) overlaps
     // chunk k's kernels (caller's stream), and chunk k's results return while k+1 computes.
-    const bool tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA);
+    const bool tag_ok = tag_max_score(sc.alphabet) > 0 && (K16 <= 16 || sc.alphabet == SW_ALPHABET_PROTEIN);
     double total_cells = 0;
     for (int64_t p = 0; p < n_pairs; ++p)
         total_cells += (double)(q_offsets[p + 1] - q_offsets[p]) * (double)(r_offsets[p + 1] - r_offsets[p]);
@@ -1002,7 +1004,7 @@ sw_status_t sw_align_batch_host(sw_handle_t h, const uint8_t* queries, const int
             hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
             if (n == 0 || m == 0) continue;
             const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
-            const int route = (s16_ok && tag_ok && (int64_t)sc.max_sigma * n <= TAG_MAX_SCORE) ? ROUTE_TAG
+            const int route = (s16_ok && tag_ok && (int64_t)sc.max_sigma * n <= tag_max_score(sc.alphabet)) ? ROUTE_TAG
                             : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
             ++hp.route_upper[route];
         }
@@ -1123,7 +1125,7 @@ sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t*
     hp.lo = 0; hp.hi = n_pairs; hp.slot = 0; hp.reset_cumulative = true;
     hp.max_n = 0; hp.max_m = 0;
     for (int r = 0; r < N_ROUTES; ++r) hp.route_upper[r] = 0;
-    const bool tag_ok = (K16 <= 16 && sc.alphabet == SW_ALPHABET_DNA);
+    const bool tag_ok = tag_max_score(sc.alphabet) > 0 && (K16 <= 16 || sc.alphabet == SW_ALPHABET_PROTEIN);
     for (int64_t p = 0; p < n_pairs; ++p) {
         const int64_t n = q_offsets[p + 1] - q_offsets[p], m = r_offsets[p + 1] - r_offsets[p];
         if (n < 0 || m < 0) return fail(h, SW_ERR_INVALID_ARGUMENT, "offsets are not non-decreasing");
@@ -1132,7 +1134,7 @@ sw_status_t sw_submit_host(sw_handle_t h, const uint8_t* queries, const int64_t*
         hp.max_m = std::max<int32_t>(hp.max_m, (int32_t)m);
         if (n == 0 || m == 0) continue;
         const int64_t smax = (int64_t)sc.max_sigma * std::min(n, m);
-        const int route = (s16_ok && tag_ok && (int64_t)sc.max_sigma * n <= TAG_MAX_SCORE) ? ROUTE_TAG
+        const int route = (s16_ok && tag_ok && (int64_t)sc.max_sigma * n <= tag_max_score(sc.alphabet)) ? ROUTE_TAG
                         : (s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
         ++hp.route_upper[route];
     }

@@ -34,6 +34,15 @@ constexpr int ROUTE_TAG = 0, ROUTE_S16 = 1, ROUTE_S32 = 2, N_ROUTES = 3;
 // s16 lanes hold Hb = H - o; the int8 profile already forces -o <= 126 (s - o <= 127, s >= 1)
 constexpr int S16_MAX_SCORE = 32000;  // Hb <= 32126 < 32768
 constexpr int TAG_MAX_SCORE = 511;    // 511 * 64 + 63 < 32768 (6 tag bits: column-in-block, row)
+#ifndef SW_PTAG
+#define SW_PTAG 0
+#endif
+// protein forward TAG (sw_wavefront.cuh PT): 8191 * 8 + 7 <= 65535 (3 row-tag bits, unsigned running max)
+constexpr int PTAG_MAX_SCORE = 8191;
+// largest max_s * n of a pair on the forward TAG route of an alphabet (-1: no TAG route)
+__host__ __device__ constexpr int tag_max_score(int alphabet) {
+    return alphabet == SW_ALPHABET_DNA ? TAG_MAX_SCORE : (SW_PTAG ? PTAG_MAX_SCORE : -1);
+}
 // Work keys: [31:30] 3 - route (0 = trivial / invalid), [29:16] stripes, [15:0] columns
 __host__ __device__ constexpr uint32_t route_key(int route) { return (uint32_t)(3 - route) << 30; }
 

@@ -25,6 +25,7 @@ struct FinishParams {
     uint32_t* hist;                 // bin histogram (zero on entry)
     int rows_s16, rows_s32;
     int max_sigma, gap_open, gap_extend;
+    int protein;
     int band_ok;                    // DNA TAG batches: narrow-band pairs take the banded reverse kernels (sw_band.cuh)
     const uint8_t* qcode;           // query codes (band pairs' reversed query prefixes)
     uint8_t* bslots;                // band buffer (sw_band.cuh): pair p's slot at (p + 1) * BAND_SLOT
@@ -116,7 +117,8 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                 }
                 int route = flag_route(fl);
                 // TAG reverse items need H <= 511 in every swept cell, also past the rectangle
-                if (route == ROUTE_TAG && (long long)P.max_sigma * n2 > TAG_MAX_SCORE) route = ROUTE_S16;
+                // (protein TAG pairs -- forward only, sw_wavefront.cuh PT -- all take the S16 reverse kernel)
+                if (route == ROUTE_TAG && (P.protein || (long long)P.max_sigma * n2 > TAG_MAX_SCORE)) route = ROUTE_S16;
                 // banded reverse pass (sw_band.cuh) when the pair's score-S paths fit 32 / 64 diagonals
                 // and its rrev region has room for the selectors the kernel reads
                 if (route == ROUTE_TAG && P.band_ok && n2 <= BAND_MAX_N2) {

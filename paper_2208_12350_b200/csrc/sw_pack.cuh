@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
                 const int64_t smax = (int64_t)P.max_sigma * (int64_t)min(nn, mm);
                 // TAG: every cell a sweep over this query can compute (also past the reference, in
                 // the columns of a longer reference of the work item) has H <= max_s * n <= 511
-                const int route = (P.s16_ok && P.tag_ok && (int64_t)P.max_sigma * nn <= TAG_MAX_SCORE) ? ROUTE_TAG
+                const int route = (P.s16_ok && P.tag_ok && (int64_t)P.max_sigma * nn <= tag_max_score(P.alphabet)) ? ROUTE_TAG
                                 : (P.s16_ok && smax <= S16_MAX_SCORE) ? ROUTE_S16 : ROUTE_S32;
                 fl = route_flag(route);
                 if (nn > 0 && mm > 0) {

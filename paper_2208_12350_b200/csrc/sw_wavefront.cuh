@@ -71,6 +71,12 @@
 #define SW_IMPROVE_VOTE 0  // 1: non-TAG forward with a warp-uniform improvement branch (vote) + predicated per-half
                            // stores (measured slower: c3 forward 3.14 vs 3.23 TCUPS, c5 3.63 vs 3.86)
 #endif
+#ifndef SW_IMERGE
+#define SW_IMERGE 0        // 1: DNA TAG forward with a 32-bit-per-row profile, halves merged by one IMAD (FMA pipe)
+#endif
+#ifndef SW_PTAG
+#define SW_PTAG 0          // 1 (measured slower): protein forward on the TAG route, 3-bit row tags, unsigned running max
+#endif
 #ifndef SW_PROT_T4
 #define SW_PROT_T4 1       // protein profile build from a transposed (s - o) table with byte transposes
 #endif
@@ -152,16 +158,19 @@ struct WaveParams {
     uint32_t sixteen;           // = 16 (opaque: IMAD.HI extraction stays on the FMA pipe)
 };
 
-template <int W, int K, class T>
+template <int W, int K, class T, bool IM = false>
 struct Geometry {
     static constexpr int SEGS = 32 / W;
     static constexpr int SLOTS = SEGS * T::NH;
     static constexpr int ROWS = W * K;                       // rows per stripe
     // profile bytes per (slot, code, lane): int8 x K (s16x2) or int32 x K (s32), 16 B aligned
     // int8 profile: 4/8/16-byte entries (one LDS.32/.64/.128 per 4/8/16 rows); int32: 16-byte multiples
-    static constexpr int PB = (T::NH == 2) ? (K <= 4 ? 4 : K <= 8 ? 8 : 16 * ((K + 15) / 16)) : 16 * ((4 * K + 15) / 16);
+    // IM (SW_IMERGE, DNA TAG forward): one 32-bit word per row, the value in its half's 16 bits (8 B aligned:
+    // LDS.64, conflict-free at a 40-byte lane stride)
+    static constexpr int PB = IM ? 4 * K : (T::NH == 2) ? (K <= 4 ? 4 : K <= 8 ? 8 : 16 * ((K + 15) / 16)) : 16 * ((4 * K + 15) / 16);
     static constexpr int PWORDS = PB / 4;
-    static constexpr int SVB = 16 * ((4 * K + 15) / 16);    // saved improvement column per (lane, half)
+    // saved improvement column per (lane, half); the lazy TAG commit keeps only (block start, raw max)
+    static constexpr int SVB = IM ? 16 : 16 * ((4 * K + 15) / 16);
     // saved columns are stored quad-major across the warp's lanes: quad w of (half h, lane l) at
     // h * SVH + w * SV_QSTRIDE + l * 16, so a warp-wide STS.128 / LDS.128 touches 32 consecutive
     // 16-byte chunks (no bank conflicts; a lane-major 64-96 B stride conflicts 4-way)
@@ -295,7 +304,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                                       const int scr_cols, const int c_lo,
                                       const volatile unsigned long long* flag_in = nullptr, unsigned long long need_base = 0,
                                       volatile unsigned long long* flag_out = nullptr, unsigned long long pub_base = 0) {
-    using G = Geometry<W, K, T>;
+    constexpr bool IM = SW_IMERGE && SW_TAG_LAZY && TAG && !REV && T::NH == 2 && K == 10;
+    using G = Geometry<W, K, T, IM>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
     constexpr int U = TAG ? (K <= 16 ? 4 : 2) : SW_UNROLL;  // column unroll (codes prefetched one block ahead)
@@ -316,11 +326,18 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     // the block and the smallest row holding it (reading R5).  Bookkeeping happens once per
     // block; afterwards the 6 tag bits are set to ones so a later column with the same H never
     // counts as an improvement.  Valid while H <= 511 (route eligibility).
-    // 6 tag bits: RB for the row (K <= 2^RB), the rest for the column within the block
-    constexpr int RB = K <= 16 ? 4 : 5;
-    constexpr int UB = 6 - RB;
-    static_assert(!TAG || ((U <= (1 << UB)) && K <= (1 << RB) && NH == 2), "TAG route geometry");
-    constexpr uint32_t TAGSET = 0x003f003fu;
+    // 6 tag bits: RB for the row (K <= 2^RB), the rest for the column within the block.
+    // PT (protein forward, SW_PTAG): 3 row bits and a commit every column, the running max taken
+    // unsigned: X * 8 + tag <= 65535 while X <= 8191 (route rule max_s * n <= PTAG_MAX_SCORE)
+    constexpr bool PT = SW_PTAG && TAG && !REV && K == 8 && NH == 2;
+    static_assert(!PT || SW_TAG_LAZY, "protein TAG needs the lazy commit");
+    constexpr int RB = PT ? 3 : K <= 16 ? 4 : 5;
+    constexpr int UB = PT ? 0 : 6 - RB;
+    constexpr int UC = PT ? 1 : U;  // columns per tag commit
+    static_assert(!TAG || ((UC <= (1 << UB)) && K <= (1 << RB) && NH == 2), "TAG route geometry");
+    constexpr uint32_t TAGSET = ((1u << (RB + UB)) - 1u) * 0x10001u;
+    // tagged value of a half (unsigned for PT)
+    auto tget = [](uint32_t v, int h) -> int { return PT ? (int)((v >> (16 * h)) & 0xffffu) : T::get(v, h); };
     uint32_t best = TAG ? TAGSET : 0u;
     int brow[NH];                        // TAG: row of the half's last improvement
     int bc[NH];                          // column of the last strict improvement, per half
@@ -357,14 +374,14 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     const uint32_t b0 = (SW_XFORM && L == 0) ? o2s : 0u;
 
     auto emit = [&](int h) {  // forward result of half h for this lane and stripe
-        const int b = TAG ? (T::get(best, h) >> 6) : T::get(best, h);
+        const int b = TAG ? (tget(best, h) >> (RB + UB)) : T::get(best, h);
         if (TAG && SW_TAG_LAZY) {
             uint32_t t0s, raw;
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t0s), "=r"(raw) : "r"(sv[h]) : "memory");
             bt0[h] = (int)t0s;
             btag[h] = raw;
-            const int v = T::get(btag[h], h);
-            bc[h] = bt0[h] + (U - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
+            const int v = tget(btag[h], h);
+            bc[h] = bt0[h] + (UC - 1 - ((v >> RB) & ((1 << UB) - 1))) - L;
             brow[h] = ((1 << RB) - 1) - (v & ((1 << RB) - 1));
         }
         if (h_pid[h] >= 0 && b > 0) {
@@ -521,6 +538,18 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
                 const uint32_t code = C4 ? __umulhi(v4[h] << (28 - 4 * u), sixteen) : cd[u % CD][h];
+                if (IM) {
+                    const uint32_t src = prof_h[h] + code * cs;
+#pragma unroll
+                    for (int q2 = 0; q2 < K / 2; ++q2) {
+                        uint32_t a, b;
+                        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(src + 8 * q2));
+                        pw[h][2 * q2] = a;
+                        pw[h][2 * q2 + 1] = b;
+                    }
+                    cd[u % CD][h] = ld_code(rp[h] + t + CD);
+                    continue;
+                }
 #ifdef SW_BAND_CHECK
                 if (SW_BAND_CHECK && code >= (uint32_t)nc) {
                     printf("wave code %u >= nc: REV %d route %d pid %d t %d L %d\n", code, (int)REV, P.route, h_pid[h], t, L);
@@ -560,6 +589,8 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 uint32_t sc;
                 if (NH == 2 && (SW_ABLATE & 2)) {
                     sc = pw[r & 1][r >> 2];  // timing ablation only: wrong scores
+                } else if (IM) {
+                    sc = pw[NH - 1][r] * one + pw[0][r];  // IMAD: halves' 16-bit values, no carry
                 } else if (NH == 2) {
                     constexpr uint32_t SEL[4] = {0xC480u, 0xD591u, 0xE6A2u, 0xF7B3u};
                     sc = prmt(pw[0][r >> 2], pw[NH - 1][r >> 2], SEL[r & 3]);
@@ -644,12 +675,17 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                     xv = HO[r];
                 }
                 // TAG: value*64 + tag per half, one IMAD on the FMA pipe (value <= 511: no carry)
-                H[r] = TAG ? xv * P.tag_mul + (uint32_t)((U - 1 - u) * (1 << RB) + (1 << RB) - 1 - r) * 0x10001u : xv;
+                H[r] = TAG ? xv * P.tag_mul + (uint32_t)((PT ? 0 : (U - 1 - u) * (1 << RB)) + (1 << RB) - 1 - r) * 0x10001u : xv;
             }
             hoLast = HO[K - 1];
             fLast = F;
             // running max over the lane's rows; strict improvement -> remember column + HO values
-            if (TAG) {
+            if (PT) {
+#pragma unroll
+                for (int r = 0; r + 1 < K; r += 2) nbt = __vimax3_u16x2(nbt, H[r], H[r + 1]);
+                tag_commit(nbt, t);  // every column (the tag names the row only)
+                nbt = best;
+            } else if (TAG) {
 #pragma unroll
                 for (int r = 0; r + 1 < K; r += 2) nbt = T::max3(nbt, H[r], H[r + 1]);
                 if (K & 1) nbt = T::max2(nbt, H[K - 1]);
@@ -720,12 +756,12 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 }
             }
             if (EV && t == next_ev) {
-                if (TAG) tag_commit(nbt, t0);  // make best / bc / brow current before emitting
+                if (TAG && !PT) tag_commit(nbt, t0);  // make best / bc / brow current before emitting
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     if (ev[h] == t) {
                         emit(h);
-                        best = T::set(best, h, T::FROZEN);
+                        best = T::set(best, h, PT ? 0xffff : T::FROZEN);
                         ev[h] = 0x7fffffff;
                     }
                 }
@@ -735,7 +771,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             }
             if (st_lane) scr_out[t - (W - 1)] = make_uint2(hoLast, fLast);
         }
-        if (TAG && !REV && (SW_TAG_LAZY || nbt != best)) tag_commit(nbt, t0);
+        if (TAG && !PT && !REV && (SW_TAG_LAZY || nbt != best)) tag_commit(nbt, t0);
         if (TAG && REV) {
             const uint32_t x = T::max2(nbt, tgt64) ^ nbt;  // zero half: block max >= S*64
             if (((x - 0x00010001u) & ~x & 0x80008000u) != 0u) rev_tag_find(nbt, t0);
@@ -929,7 +965,8 @@ __device__ __forceinline__ int sweep_skew2(const WaveParams& P, const uint8_t* p
 template <class T, int W, int K, bool REV, bool TAG, bool LIN>
 __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
     wavefront_kernel(const WaveParams P) {
-    using G = Geometry<W, K, T>;
+    constexpr bool IMK = SW_IMERGE && SW_TAG_LAZY && TAG && !REV && T::NH == 2 && K == 10;
+    using G = Geometry<W, K, T, IMK>;
     constexpr int NH = T::NH;
     constexpr int SLOTS = G::SLOTS;
     // Row/column tags (H*64 + tag) need H <= 511 in every computed cell, also past a half's
@@ -1097,7 +1134,17 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
                     const int l = (cb / G::PWORDS) % W;
                     const int w = cb % G::PWORDS;
                     uint8_t* base = prof + (size_t)sl * nc * W * G::PB + (size_t)l * G::PB + w * 4;
-                    if (NH == 2 && P.sc.alphabet == SW_ALPHABET_DNA) {
+                    if (IMK) {
+                        // one word per row: (s - o) in the slot's half (low half: zero-extended; high half:
+                        // low 16 bits zero), -128 for rows without a residue and for the pad code
+                        const int i = row0 + l * K + w;
+                        const int qc = (pid >= 0 && i < n) ? P.qcode[REV ? qp + n - 1 - i : qp + i] : -1;
+                        const int sh = 16 * (sl % NH);
+                        for (int c = 0; c < nc; ++c) {
+                            const int v = (qc >= 0 && c < nc - 1) ? (qc == c ? P.sc.match : P.sc.mismatch) - o : -128;
+                            *reinterpret_cast<uint32_t*>(base + (size_t)c * W * G::PB) = ((uint32_t)v & 0xffffu) << sh;
+                        }
+                    } else if (NH == 2 && P.sc.alphabet == SW_ALPHABET_DNA) {
                         // DNA: s(q, c) is match / mismatch, four rows per word with byte-SIMD
                         uint32_t q4 = 0u, inv = 0u;  // query codes; 0xff bytes for rows without a residue
 #pragma unroll
