@@ -107,11 +107,13 @@ typedef struct {
  * on the handle.  Flag SW_MODE_NO_BAND keeps every reverse-pass pair on the
  * row-sweep kernels instead of the banded reverse kernels (DNA pairs whose
  * score-S paths fit 32 / 64 diagonals; identical results --
- * comparison and testing).  Errors: SW_ERR_INVALID_ARGUMENT for an unknown
- * mode bit.
+ * comparison and testing); batches (host-call chunks) of fewer than 16,384
+ * pairs use the row-sweep kernels anyway (too few work items to fill the GPU)
+ * unless flag SW_MODE_BAND_ALWAYS is set (testing).  Errors:
+ * SW_ERR_INVALID_ARGUMENT for an unknown mode bit.
  */
 typedef enum { SW_MODE_FULL = 0, SW_MODE_END_ONLY = 1, SW_MODE_AFFINE_ONLY = 2, SW_MODE_TB_INT32 = 4,
-               SW_MODE_POISON = 8, SW_MODE_NO_BAND = 16 } sw_mode_t;
+               SW_MODE_POISON = 8, SW_MODE_NO_BAND = 16, SW_MODE_BAND_ALWAYS = 32 } sw_mode_t;
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode);
 
 /*

@@ -664,7 +664,10 @@ sw_status_t align_impl(sw_context* h, const uint8_t* queries, const int64_t* q_o
     F.qpos = h->qpos.p; F.rpos = h->rpos.p; F.nlen_rev = h->nlen_rev.p; F.mlen_rev = h->mlen_rev.p;
     F.target = h->target.p; F.key_rev = h->key.p; F.hist = hist; F.rows_s16 = rows16; F.rows_s32 = rows32;
     F.max_sigma = sc.max_sigma; F.gap_open = sc.gap_open; F.gap_extend = sc.gap_extend; F.pad_code = (uint8_t)(sc.nc - 1);
-    const bool band_ok = !protein && s16_ok && K16 <= 16 && !(h->mode & SW_MODE_NO_BAND);
+    // banded reverse pass (sw_band.cuh): a work item holds 16 / 32 pairs and sweeps ~2 n2 + 64 steps, so a
+    // small batch (c1: 1,000 pairs) leaves most SMs idle on it -- the row sweep (4 pairs per item) is faster there
+    const bool band_ok = !protein && s16_ok && K16 <= 16 && !(h->mode & SW_MODE_NO_BAND) &&
+                         ((hi - lo) >= BAND_MIN_PAIRS || (h->mode & SW_MODE_BAND_ALWAYS));
     F.band_ok = band_ok ? 1 : 0; F.protein = protein ? 1 : 0; F.qcode = h->qcode.p; F.bslots = h->bslots.p;
     F.rrev_bytes = (int64_t)h->rrev.cap; F.band_bytes = (int64_t)h->bslots.cap;
     F.out = *out; F.stats = stats; F.end_only = end_only ? 1 : 0; F.rev_small = small_rev ? 1 : 0;
@@ -1100,7 +1103,7 @@ sw_status_t sw_traceback(sw_handle_t h, const uint8_t* queries, const int64_t* q
 
 sw_status_t sw_set_mode(sw_handle_t h, int32_t mode) {
     if (!h) return SW_ERR_INVALID_ARGUMENT;
-    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32 | SW_MODE_POISON | SW_MODE_NO_BAND))
+    if (mode & ~(SW_MODE_END_ONLY | SW_MODE_AFFINE_ONLY | SW_MODE_TB_INT32 | SW_MODE_POISON | SW_MODE_NO_BAND | SW_MODE_BAND_ALWAYS))
         return fail(h, SW_ERR_INVALID_ARGUMENT, "unknown mode");
     h->mode = mode;
     return SW_OK;

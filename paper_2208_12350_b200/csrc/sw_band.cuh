@@ -56,6 +56,10 @@ constexpr int BAND_SLOT = 576;
 constexpr int BAND_ROFF = QREV_STRIDE + 32;
 // longest reversed query of a band pair: the kernel reads q' up to i < n2 + CAP/2 + 15 (< QREV_STRIDE - QREV_PAD)
 constexpr int BAND_MAX_N2 = 176;
+#ifndef SW_BAND_MIN_PAIRS
+#define SW_BAND_MIN_PAIRS 16384
+#endif
+constexpr int64_t BAND_MIN_PAIRS = SW_BAND_MIN_PAIRS;  // batches (chunks) below this keep the row-sweep reverse pass
 constexpr int BAND_DLO_ALIGN = 8;     // dlo = -DI rounded down to a multiple of 8 (aligned reference words)
 constexpr int BAND_JPAD = 16;         // selector bytes written for j' < n2 + CAP + BAND_JPAD
 constexpr uint8_t SEL_PAD = 0x88;     // A-form selector of a pad reference code (sign of byte 0, twice)

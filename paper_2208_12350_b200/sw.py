@@ -35,6 +35,7 @@ SW_MODE_AFFINE_ONLY = 2
 SW_MODE_TB_INT32 = 4
 SW_MODE_POISON = 8
 SW_MODE_NO_BAND = 16
+SW_MODE_BAND_ALWAYS = 32
 
 EXPORTED = ("sw_init", "sw_reserve", "sw_align_batch", "sw_align_query_db", "sw_align_batch_host", "sw_submit_host", "sw_wait", "sw_set_mode", "sw_traceback", "sw_batch_status", "sw_free",
             "sw_status_string", "sw_last_error_message", "sw_plan_shards", "sw_enable_stage_timing",

@@ -932,8 +932,14 @@ def test_reverse_gap_band_edges(aligner, scoring):
         r = np.concatenate([fl[0], r, fl[1]])
         pairs.append(("".join(q), "".join(r)))
     b = synth.from_pairs(pairs, sc)
-    assert_parity(aligner.align(b), oracle_batch(b), b)
-    assert aligner.batch_status()[0] == sw.SW_OK
+    exp = oracle_batch(b)
+    try:
+        for mode in (sw.SW_MODE_FULL, sw.SW_MODE_BAND_ALWAYS):  # row-sweep and banded reverse kernels
+            aligner.set_mode(mode)
+            assert_parity(aligner.align(b), exp, b)
+            assert aligner.batch_status()[0] == sw.SW_OK
+    finally:
+        aligner.set_mode(sw.SW_MODE_FULL)
 
 
 @pytest.mark.parametrize("kind", ["c2", "c1_scorings", "repeats", "indels"])
@@ -986,7 +992,7 @@ def test_banded_reverse_matches_row_sweep(kind):
             a.set_mode(sw.SW_MODE_NO_BAND)
             got_rows = a.align(b)
             rev_rows = a.reverse_cells()
-            a.set_mode(sw.SW_MODE_FULL)
+            a.set_mode(sw.SW_MODE_BAND_ALWAYS)  # below the 16,384-pair default threshold
             got_band = a.align(b)
             rev_band = a.reverse_cells()
             assert_parity(got_rows, exp, b)
@@ -994,5 +1000,7 @@ def test_banded_reverse_matches_row_sweep(kind):
             assert a.batch_status()[0] == sw.SW_OK
             if kind == "c2":
                 assert rev_band < 0.6 * rev_rows, (rev_band, rev_rows)
+            a.set_mode(sw.SW_MODE_FULL)
+            assert_parity(a.align(b), exp, b)  # default mode (row sweep for batches this small)
     finally:
         a.close()

@@ -133,7 +133,9 @@ def soak_invariance(seed, budget):
         while time.time() - t0 < budget:
             sc = random_scoring(rng)
             b = fast_batch(rng, sc, int(rng.integers(500, 6000)))
+            a.set_mode(sw.SW_MODE_BAND_ALWAYS)  # the whole batch on the banded reverse kernels (DNA) ...
             ref = a.align(b)
+            a.set_mode(sw.SW_MODE_FULL if rng.random() < 0.5 else sw.SW_MODE_BAND_ALWAYS)  # ... the rest either way
             perm = rng.permutation(b.n_pairs)
             got = a.align(b.subset(perm))
             inv = {f: np.empty_like(ref[f]) for f in FIELDS}
@@ -191,6 +193,9 @@ def main():
         while time.time() - t0 < budget:
             sc = random_scoring(rng)
             b = batch(rng, sc)
+            # half of the batches force the banded reverse kernels (DNA; batches this small use the row
+            # sweep by default)
+            a.set_mode(sw.SW_MODE_BAND_ALWAYS if rng.random() < 0.5 else sw.SW_MODE_FULL)
             exp = oracle.align_batch(b.queries, b.q_offsets, b.refs, b.r_offsets, b.scoring)
             with_paths = rng.random() < 0.5
             if with_paths:
