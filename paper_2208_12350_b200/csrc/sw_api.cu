@@ -35,12 +35,6 @@ namespace {
 constexpr int W16 = SW_W16, K16 = SW_K16;
 // protein: 8 rows per lane keep the 25-code int8 profile at 8 bytes per (code, lane) -> 12.8 KB per
 // warp, so shared memory allows 16 resident warps per SM (10 rows would need 16-byte entries)
-#ifndef SW_KP
-#define SW_KP 8
-#endif
-#ifndef SW_WP
-#define SW_WP 16
-#endif
 constexpr int WP = SW_WP, KP = SW_KP;
 constexpr int W32 = 16, K32 = 10;
 constexpr int WARPS_PER_BLOCK = 4;
@@ -303,8 +297,8 @@ void plan_waves(const sw_context* h, const Scoring& sc, bool protein, const Batc
             lr[r] = plan_wave<G32>(h, krev[r], sc.nc, rev_upper);
         } else if (protein) {
             // 3-warp blocks: 5 blocks x 3 warps fit the SM's shared memory (4-warp blocks: only 3)
-            lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], 3);
-            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, rev_upper, 3);
+            lf[r] = plan_wave<GP>(h, kfwd[r], sc.nc, hs.fwd_count[r], SW_PROT_THREADS / 32);
+            lr[r] = plan_wave<GP>(h, krev[r], sc.nc, rev_upper, SW_PROT_THREADS / 32);
         } else {
             lf[r] = r == ROUTE_TAG ? plan_wave<G16F>(h, kfwd[r], sc.nc, hs.fwd_count[r])
                                    : plan_wave<G16>(h, kfwd[r], sc.nc, hs.fwd_count[r]);

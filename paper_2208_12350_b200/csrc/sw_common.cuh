@@ -33,6 +33,13 @@ constexpr uint8_t CODE_BAD = 0xff;
 constexpr int ROUTE_TAG = 0, ROUTE_S16 = 1, ROUTE_S32 = 2, N_ROUTES = 3;
 // s16 lanes hold Hb = H - o; the int8 profile already forces -o <= 126 (s - o <= 127, s >= 1)
 constexpr int S16_MAX_SCORE = 32000;  // Hb <= 32126 < 32768
+// protein geometry (sw_api.cu): 8 rows per lane keep the 25-code int8 profile at 8 bytes per (code, lane)
+#ifndef SW_KP
+#define SW_KP 8
+#endif
+#ifndef SW_WP
+#define SW_WP 16
+#endif
 constexpr int TAG_MAX_SCORE = 511;    // 511 * 64 + 63 < 32768 (6 tag bits: column-in-block, row)
 #ifndef SW_PTAG
 #define SW_PTAG 0

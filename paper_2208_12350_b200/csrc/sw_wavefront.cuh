@@ -329,7 +329,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
     // 6 tag bits: RB for the row (K <= 2^RB), the rest for the column within the block.
     // PT (protein forward, SW_PTAG): 3 row bits and a commit every column, the running max taken
     // unsigned: X * 8 + tag <= 65535 while X <= 8191 (route rule max_s * n <= PTAG_MAX_SCORE)
-    constexpr bool PT = SW_PTAG && TAG && !REV && K == 8 && NH == 2;
+    constexpr bool PT = SW_PTAG && TAG && !REV && K == 8 && K == SW_KP && NH == 2;
     static_assert(!PT || SW_TAG_LAZY, "protein TAG needs the lazy commit");
     constexpr int RB = PT ? 3 : K <= 16 ? 4 : 5;
     constexpr int UB = PT ? 0 : 6 - RB;
@@ -963,7 +963,7 @@ __device__ __forceinline__ int sweep_skew2(const WaveParams& P, const uint8_t* p
 }
 
 template <class T, int W, int K, bool REV, bool TAG, bool LIN>
-__global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
+__global__ void __launch_bounds__((K == SW_KP && W == SW_WP) ? SW_PROT_THREADS : 128, (K == SW_KP && W == SW_WP) ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
     wavefront_kernel(const WaveParams P) {
     constexpr bool IMK = SW_IMERGE && SW_TAG_LAZY && TAG && !REV && T::NH == 2 && K == 10;
     using G = Geometry<W, K, T, IMK>;
@@ -981,12 +981,12 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
     // protein s16x2 profiles: (s - o) bytes of query residue a against codes 4q..4q+3 in word
     // s_t4[a][q]; row a = 24 is the pad residue (-128 against every code), code 24 the pad code
     constexpr int TQ = (NC_PROTEIN + 3) / 4;
-    __shared__ uint32_t s_t4[SW_T4_ALL || K == 8 ? 25 * TQ : 1];  // K == 8: the protein geometry
+    __shared__ uint32_t s_t4[SW_T4_ALL || K == SW_KP ? 25 * TQ : 1];  // K == SW_KP: the protein geometry
     for (int k = threadIdx.x; k < 24 * 24; k += blockDim.x) {
         const int a = k / 24, b = k % 24;
         s_sigma[k] = (int8_t)(P.sc.alphabet == SW_ALPHABET_DNA ? 0 : c_blosum62[a][b]);
     }
-    if (NH == 2 && (SW_T4_ALL || K == 8) && P.sc.alphabet != SW_ALPHABET_DNA) {
+    if (NH == 2 && (SW_T4_ALL || K == SW_KP) && P.sc.alphabet != SW_ALPHABET_DNA) {
         for (int k = threadIdx.x; k < 25 * TQ; k += blockDim.x) {
             const int a = k / TQ, q = k % TQ;
             uint32_t word = 0u;
@@ -1166,7 +1166,7 @@ __global__ void __launch_bounds__(K == 8 ? SW_PROT_THREADS : 128, K == 8 ? SW_PR
                             *reinterpret_cast<uint32_t*>(base + (size_t)c * W * G::PB) = word;
                         }
                         *reinterpret_cast<uint32_t*>(base + (size_t)(nc - 1) * W * G::PB) = padw;
-                    } else if (NH == 2 && SW_PROT_T4 && (SW_T4_ALL || K == 8)) {
+                    } else if (NH == 2 && SW_PROT_T4 && (SW_T4_ALL || K == SW_KP)) {
                         // protein: four rows' residues index the transposed table; a 4x4 byte
                         // transpose (8 PRMT) turns four table words into the words of four codes
                         uint32_t qa[4];

@@ -34,8 +34,11 @@ VAR = os.path.join(ROOT, "build_var", "gevo")
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles", "gevo")
 
-# tunable -> allowed values (the first is the shipped default)
-SPACE = {
+# tunable -> allowed values (the first is the shipped default).  Two targets: the DNA geometry (fitness:
+# c2 GCUPS) and, with GEVO_TARGET=protein, the protein path (fitness: c3 GCUPS) -- rows / lanes of the
+# 25-code int8 profile, block shape, code prefetch, column unroll and the improvement-recording forms
+TARGET = os.environ.get("GEVO_TARGET", "dna")
+SPACE_DNA = {
     "SW_K16": [10, 8, 12, 16],
     "SW_W16": [16, 8],
     "SW_CODE_DIST": [4, 1, 2],
@@ -43,10 +46,32 @@ SPACE = {
     "SW_MIN_BLOCKS": [4, 3, 5],
     "SW_BODY_BLOCKS": [2, 1],
 }
+SPACE_PROTEIN = {
+    "SW_KP": [8, 6, 4],
+    "SW_WP": [16, 8],
+    "SW_PROT_THREADS": [96, 64, 128, 32],
+    "SW_PROT_BLOCKS": [5, 7, 3, 4, 15],
+    "SW_CODE_DIST": [4, 1, 2],
+    "SW_UNROLL": [4, 2, 8],
+    "SW_IMPROVE_VOTE": [0, 1],
+    "SW_PRED_IMPROVE": [0, 1],
+    "SW_PTAG": [0, 1],
+}
+SPACE = SPACE_PROTEIN if TARGET == "protein" else SPACE_DNA
+FIT = "c3" if TARGET == "protein" else "c2"
+TAG = "p" if TARGET == "protein" else ""
 POP = 10
 
 
 def valid(g: dict) -> bool:
+    if TARGET == "protein":
+        rows = g["SW_KP"] * g["SW_WP"]
+        warps = g["SW_PROT_THREADS"] // 32 * g["SW_PROT_BLOCKS"]
+        if g["SW_UNROLL"] % g["SW_CODE_DIST"] or not (64 <= rows <= 128) or warps > 15 or warps < 8:
+            return False        # shared memory (12.8 KB profile per warp) holds at most 15 warps per SM
+        if g["SW_PTAG"] and (g["SW_KP"] != 8 or g["SW_IMPROVE_VOTE"] or g["SW_PRED_IMPROVE"]):
+            return False        # the protein TAG form is the 8-row geometry and has no improvement branch
+        return not (g["SW_IMPROVE_VOTE"] and g["SW_PRED_IMPROVE"])
     rows = g["SW_K16"] * g["SW_W16"]
     if g["SW_UNROLL"] % g["SW_CODE_DIST"]:
         return False            # static_assert since generations 0-1, whose parity gate rejected distance 3
@@ -80,7 +105,7 @@ def crossover(a: dict, b: dict, rng: random.Random) -> dict:
 
 
 def genomes_path(gen: int) -> str:
-    return os.path.join(VAR, f"g{gen}.json")
+    return os.path.join(VAR, f"{TAG}g{gen}.json")
 
 
 def cmd_build(gen: int):
@@ -93,7 +118,7 @@ def cmd_build(gen: int):
             if key(c) not in {key(x) for x in pop}:
                 pop.append(c)
     else:
-        sel = json.load(open(os.path.join(PROF, f"select_g{gen - 1}.json")))
+        sel = json.load(open(os.path.join(PROF, f"select_{TAG}g{gen - 1}.json")))
         parents = sel["parents"]
         seen = set(sel["evaluated"])
         pop = [parents[0]]  # elitism
@@ -107,7 +132,7 @@ def cmd_build(gen: int):
     from paper_2208_12350_b200 import _build
 
     def one(g):
-        out = os.path.join(VAR, f"g{gen}_{key(g)}.so")
+        out = os.path.join(VAR, f"{TAG}g{gen}_{key(g)}.so")
         if not os.path.exists(out):
             _build.build(force=True, out=out, defines=[f"{k}={v}" for k, v in g.items()])
         return out
@@ -125,7 +150,7 @@ sys.path.insert(0, ".")
 from paper_2208_12350_b200 import sw, synth
 a = sw.Aligner(0); a.enable_stage_timing(True)
 res = {}
-sets = {"c2": synth.generate("c2"), "c3": synth.generate("c3", 0, 20000)}
+sets = {"c2": synth.generate("c2"), "c3": synth.generate("c3")}
 rng = np.random.default_rng(5)
 ties = synth.from_pairs([("".join(rng.choice(list("AC"), int(rng.integers(1, 300)))),
                           "".join(rng.choice(list("AC"), int(rng.integers(1, 300))))) for _ in range(400)],
@@ -140,11 +165,15 @@ for name, b in sets.items():
         e0.record(); a.align_tensors(q, qo, r, ro, b.scoring, out=out); e1.record(); e1.synchronize()
         ts.append(e0.elapsed_time(e1)); fw.append(a.stage_ms()["fwd"])
     o = out[:, :b.n_pairs].cpu().numpy()
-    keep = o[:, :2000] if name == "c2" else o[:, :300]
+    keep = o[:, :2000] if name == "c2" else o[:, :2000]
     res[name] = {"ms": float(np.median(ts)), "fwd_ms": float(np.median(fw)), "cells": b.cells(),
                  "gate": keep.astype(np.int64).tolist()}
 o = a.align(ties)
 res["ties"] = {"gate": np.stack([o[f] for f in ("score", "q_end", "r_end", "q_start", "r_start")]).astype(np.int64).tolist()}
+pties = synth.from_pairs([("".join(rng.choice(list("AW"), int(rng.integers(1, 900)))),
+                           "".join(rng.choice(list("AW"), int(rng.integers(1, 900))))) for _ in range(300)], synth.PROTEIN_SCORING)
+o = a.align(pties)
+res["pties"] = {"gate": np.stack([o[f] for f in ("score", "q_end", "r_end", "q_start", "r_start")]).astype(np.int64).tolist()}
 print("RESULT " + json.dumps(res))
 '''
 
@@ -164,11 +193,11 @@ def cmd_measure(gen: int):
                          "error": None if line else r.stderr[-800:]}
         print(name, "ok" if line else "FAILED", flush=True)
     os.makedirs(OUT, exist_ok=True)
-    json.dump(results, open(os.path.join(OUT, f"gevo_g{gen}.json"), "w"))
+    json.dump(results, open(os.path.join(OUT, f"gevo_{TAG}g{gen}.json"), "w"))
 
 
 def cmd_select(gen: int):
-    res = json.load(open(os.path.join(OUT, f"gevo_g{gen}.json")))
+    res = json.load(open(os.path.join(OUT, f"gevo_{TAG}g{gen}.json")))
     base = res["baseline"]["result"]
     rows, evaluated = [], []
     for name, d in res.items():
@@ -176,23 +205,24 @@ def cmd_select(gen: int):
             continue
         evaluated.append(name)
         r = d["result"]
-        ok = r is not None and all(r[s]["gate"] == base[s]["gate"] for s in ("c2", "c3", "ties"))
+        ok = r is not None and all(r[s]["gate"] == base[s]["gate"] for s in ("c2", "c3", "ties", "pties") if s in base)
         rows.append({"variant": name, "genome": d["genome"], "gated": ok,
                      "c2_ms": r["c2"]["ms"] if r else None, "c2_fwd_ms": r["c2"]["fwd_ms"] if r else None,
                      "c3_ms": r["c3"]["ms"] if r else None,
-                     "fitness": (r["c2"]["cells"] / r["c2"]["ms"] / 1e6) if (r and ok) else 0.0})
+                     "c3_fwd_ms": r["c3"]["fwd_ms"] if r else None,
+                     "fitness": (r[FIT]["cells"] / r[FIT]["ms"] / 1e6) if (r and ok) else 0.0})
     rows.sort(key=lambda x: -x["fitness"])
     prev = []
     if gen > 0:
-        prev = json.load(open(os.path.join(PROF, f"select_g{gen - 1}.json")))["evaluated"]
+        prev = json.load(open(os.path.join(PROF, f"select_{TAG}g{gen - 1}.json")))["evaluated"]
     parents = [x["genome"] for x in rows if x["gated"]][:3]
     os.makedirs(PROF, exist_ok=True)
     json.dump({"gen": gen, "baseline_c2_ms": base["c2"]["ms"], "baseline_c3_ms": base["c3"]["ms"],
                "rows": rows, "parents": parents or [default()], "evaluated": sorted(set(prev + evaluated))},
-              open(os.path.join(PROF, f"select_g{gen}.json"), "w"), indent=1)
+              open(os.path.join(PROF, f"select_{TAG}g{gen}.json"), "w"), indent=1)
     print(f"generation {gen}: baseline c2 {base['c2']['ms']:.3f} ms, c3 {base['c3']['ms']:.3f} ms")
     for x in rows:
-        print(f"  {x['variant']:60s} gated={x['gated']!s:5s} c2 {x['c2_ms']} ms  fwd {x['c2_fwd_ms']}  c3 {x['c3_ms']}")
+        print(f"  {x['variant']:60s} gated={x['gated']!s:5s} c2 {x['c2_ms']} ms  fwd {x['c2_fwd_ms']}  c3 {x['c3_ms']} (fwd {x['c3_fwd_ms']})")
 
 
 if __name__ == "__main__":
