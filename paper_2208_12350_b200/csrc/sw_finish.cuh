@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
     for (int64_t base = P.lo + gw * FIN_PPW; base < P.hi; base += nw * FIN_PPW) {
         const int64_t p = base + lane;
         int64_t rp = 0, w0 = 0, kb = 0, soff = 0;  // k = a - kb (reversed index), source = soff - a
-        int j = -1, cnt = 0, form = 0, band = -1, n2b = 0;
+        int j = -1, cnt = 0, form = 0, band = -1, n2b = 0, bcnt = 0;
         if (lane < FIN_PPW && p < P.hi) {
             P.keys_rev[p] = 0ull;
             const uint8_t fl = P.flags[p];
@@ -159,9 +159,10 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                     ++l_band[band];
                     // output words covering the slot's selectors j' in [-32, JW): the reversed prefix as
                     // A-form PRMT selectors, pad selectors around it (sw_band.cuh)
+                    // (written by the per-band-pair pass below, not the flat list)
                     kb = (p + 1) * BAND_SLOT + BAND_ROFF;
                     w0 = (kb - 32) >> 2;
-                    cnt = (32 + band_jw(n2, band_cap(band))) >> 2;
+                    bcnt = (32 + band_jw(n2, band_cap(band))) >> 2;
                     soff = rp + kb + j;
                     form = 1;
                 } else {
@@ -240,44 +241,82 @@ __global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
                 (ff[u] ? bdst : dst)[aa[u] >> 2] = v;
             }
         }
-        // band pairs' reversed query prefixes: the pair's whole QREV_STRIDE slot, q'[i] = q[n2 - 1 - i] at
-        // QREV_PAD + i, pad codes elsewhere; two words per lane, each one PRMT of two aligned source words
+        // Band pairs, one at a time with the whole warp: the reversed reference prefix as A-form PRMT
+        // selectors for j' in [-32, JW) (<= 72 words) and the reversed query prefix q'[i] = q[n2 - 1 - i] at
+        // QREV_PAD + i of the slot, pad codes elsewhere (64 words); every word one PRMT of two aligned source
+        // words (byte-wise masking at the prefixes' edges), all loads of the pair issued before the stores.
         unsigned bmask = __ballot_sync(FULL, lane < FIN_PPW && band >= 0);
+        const uint32_t* qs = reinterpret_cast<const uint32_t*>(P.qcode);
         while (bmask) {
-            const int src_l = __ffs(bmask) - 1;
+            const int sl = __ffs(bmask) - 1;
             bmask &= bmask - 1;
-            const int64_t bp = base + src_l;
-            const int bn2 = __shfl_sync(FULL, n2b, src_l);
+            const int64_t bp = base + sl;
+            const int64_t okb = __shfl_sync(FULL, kb, sl), osoff = __shfl_sync(FULL, soff, sl), ow0 = __shfl_sync(FULL, w0, sl);
+            const int oj = __shfl_sync(FULL, j, sl), ocnt = __shfl_sync(FULL, bcnt, sl), bn2 = __shfl_sync(FULL, n2b, sl);
             const int64_t qp = P.qpos[bp];
-            const uint32_t* qs = reinterpret_cast<const uint32_t*>(P.qcode);
-            uint32_t* qd = reinterpret_cast<uint32_t*>(P.bslots + (bp + 1) * BAND_SLOT);
+            constexpr int RW = 3, QW = 2;  // words per lane: selectors (<= 96), query slot (64)
+            uint32_t x0[RW + QW], x1[RW + QW], sl4[RW + QW];
+            int64_t sb[RW + QW];
 #pragma unroll
-            for (int w = 0; w < 2; ++w) {
-                const int x = (2 * lane + w) * 4;       // slot byte of the word's byte 0
-                const int i0 = x - QREV_PAD;            // q' index of byte 0
-                // byte b = q'[i0 + b] = qcode[qp + bn2 - 1 - i0 - b]
-                const int64_t sbeg = qp + bn2 - 1 - i0 - 3;
-                uint32_t v = 0x04040404u;
-                if (i0 + 3 >= 0 && i0 < bn2) {
-                    const int64_t sb = sbeg > 0 ? sbeg : 0;   // words entirely outside are never loaded
-                    const uint32_t o = (uint32_t)(sb & 3);
-                    const uint32_t y0 = __ldg(qs + (sb >> 2)), y1 = __ldg(qs + (sb >> 2) + 1);
-                    v = __byte_perm(y0, y1, (o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
-                    if (sbeg < 0 || i0 < 0 || i0 + 3 >= bn2) {
-                        uint32_t m = 0;
+            for (int u = 0; u < RW + QW; ++u) {
+                x0[u] = 0u; x1[u] = 0u; sl4[u] = 0u; sb[u] = -1;
+                if (u < RW) {
+                    const int g = lane + 32 * u;
+                    const int64_t a = (ow0 + g) * 4;          // band-buffer byte of the word's byte 0
+                    const int64_t sbeg = osoff - a - 3;       // rcode index of its byte 3
+                    sb[u] = sbeg;
+                    if (g < ocnt && sbeg >= 0 && a - okb <= oj) {  // (words wholly past the prefix are pads)
+                        x0[u] = __ldg(src + (sbeg >> 2));
+                        x1[u] = __ldg(src + (sbeg >> 2) + 1);
+                    }
+                } else {
+                    const int i0 = (lane + 32 * (u - RW)) * 4 - QREV_PAD;
+                    const int64_t sbeg = qp + bn2 - 1 - i0 - 3;   // qcode index of byte 3 (q'[i0 + 3])
+                    sb[u] = sbeg;
+                    if (i0 + 3 >= 0 && i0 < bn2 && sbeg >= 0) {
+                        x0[u] = __ldg(qs + (sbeg >> 2));
+                        x1[u] = __ldg(qs + (sbeg >> 2) + 1);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RW + QW; ++u) {
+                const uint32_t o = (uint32_t)(sb[u] & 3);
+                uint32_t v = __byte_perm(x0[u], x1[u], (o + 3) | ((o + 2) << 4) | ((o + 1) << 8) | (o << 12));
+                if (u < RW) {
+                    const int g = lane + 32 * u;
+                    if (g >= ocnt) continue;
+                    const int64_t a = (ow0 + g) * 4;
+                    const int64_t k0 = a - okb;
+                    if (k0 < 0 || k0 + 3 > oj) {
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if (k0 + b < 0 || k0 + b > oj) v = (v & ~(0xffu << (8 * b))) | (padw & (0xffu << (8 * b)));
+                    }
+                    const uint32_t pads = (v >> 2) & 0x01010101u;   // A-form: c * 0x11 + 0x80, pad -> SEL_PAD
+                    v = v * 0x11u + 0x80808080u - pads * 0x3cu;
+#if SW_BAND_CHECK
+                    if (a < 0 || a + 4 > P.band_bytes) { printf("finish band write out of buffer %lld\n", (long long)a); __trap(); }
+#endif
+                    bdst[a >> 2] = v;
+                } else {
+                    const int w = lane + 32 * (u - RW);
+                    const int i0 = w * 4 - QREV_PAD;
+                    if (i0 + 3 < 0 || i0 >= bn2) {
+                        v = 0x04040404u;
+                    } else if (sb[u] < 0 || i0 < 0 || i0 + 3 >= bn2) {
+                        v = 0u;
 #pragma unroll
                         for (int b = 0; b < 4; ++b) {
                             const int ib = i0 + b;
-                            const uint32_t cb = (ib >= 0 && ib < bn2) ? (uint32_t)P.qcode[qp + bn2 - 1 - ib] : 4u;
-                            m |= cb << (8 * b);
+                            v |= ((ib >= 0 && ib < bn2) ? (uint32_t)P.qcode[qp + bn2 - 1 - ib] : 4u) << (8 * b);
                         }
-                        v = m;
                     }
-                }
 #if SW_BAND_CHECK
-                if ((bp + 2) * BAND_SLOT > P.band_bytes) { printf("finish qrev write out of buffer %lld\n", (long long)bp); __trap(); }
+                    if ((bp + 2) * BAND_SLOT > P.band_bytes) { printf("finish qrev write out of buffer %lld\n", (long long)bp); __trap(); }
 #endif
-                qd[2 * lane + w] = v;
+                    reinterpret_cast<uint32_t*>(P.bslots + (bp + 1) * BAND_SLOT)[w] = v;
+                }
             }
         }
     }
