@@ -145,6 +145,14 @@ __device__ __forceinline__ uint8_t conv1(uint8_t ch, const uint8_t* lut, uint8_t
 }
 
 // Largest k in [0, cnt) with a[k] <= x (a non-decreasing; k = 0 if none).
+__device__ __forceinline__ int owner_of32(const int32_t* a, int cnt, int x) {
+    int lo = 0, hi = cnt - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a[mid] <= x) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
 __device__ __forceinline__ int owner_of(const int64_t* a, int cnt, int64_t x) {
     int lo = 0, hi = cnt - 1;
     while (lo < hi) {
@@ -197,6 +205,10 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
     __shared__ int32_t s_m[PACK_WARPS][PPW];
     __shared__ int64_t s_qa[PACK_WARPS][PPW];     // query payload starts
     __shared__ uint32_t s_badbits[PACK_WARPS];
+    __shared__ int32_t s_slot32[PACK_WARPS][PPW];        // slot start rp - PADL, relative to the warp's span base
+    __shared__ int32_t s_ylo[PACK_WARPS][PPW], s_yhi[PACK_WARPS][PPW];  // relative vector starts whose 16 source
+                                                                        // bytes lie inside the caller's payload
+    __shared__ const uint8_t* s_srcb[PACK_WARPS][PPW];   // payload address of relative code position 0
     if (threadIdx.x == 0) {
         s_bad = s_maxn = s_maxm = s_malformed = s_reject = 0;
         for (int r = 0; r < N_ROUTES; ++r) s_route[r] = 0;
@@ -255,56 +267,86 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
             // ---- references: output vectors of [lo, hi) in rcode ----
             const int64_t lo = __shfl_sync(FULL, rp, 0) - PADL;
             const int64_t hi = __shfl_sync(FULL, rp + m + PADR, cnt - 1);
-            const int64_t v_lo = lo >> 4, v_hi = (hi - 1) >> 4;
-            for (int64_t vb = v_lo; vb <= v_hi; vb += 32 * PACK_FB) {
+            // 32-bit offsets relative to the span's first 16-byte vector (a span is <= 8 references of
+            // <= 65,535 codes plus pads)
+            const int64_t base = lo & ~(int64_t)15;
+            const int nvec = (int)(((hi - 1) >> 4) - (lo >> 4)) + 1;
+            const int lo_r = (int)(lo - base), hi_r = (int)(hi - base);
+            int32_t* slot32 = s_slot32[wib];
+            int32_t* ylo = s_ylo[wib];
+            int32_t* yhi = s_yhi[wib];
+            const uint8_t** srcb = s_srcb[wib];
+            if (act) {
+                const int64_t d = (ra - rp) + base;  // payload index of relative position 0
+                slot32[lane] = (int32_t)(rp - PADL - base);
+                srcb[lane] = P.refs + d;
+                const int64_t l0 = r0 - d, l1 = rN - 16 - d;
+                ylo[lane] = (int32_t)max((int64_t)INT32_MIN, min((int64_t)INT32_MAX, l0));
+                yhi[lane] = (int32_t)max((int64_t)INT32_MIN, min((int64_t)INT32_MAX, l1));
+            }
+            __syncwarp();
+            uint8_t* rdst = P.rcode + base;
+            for (int vr = 0; vr < nvec; vr += 32 * PACK_FB) {
                 uint4 src[PACK_FB];
                 int rs[PACK_FB], re[PACK_FB], kk[PACK_FB];
 #pragma unroll
                 for (int u = 0; u < PACK_FB; ++u) {
-                    const int64_t y0 = (vb + u * 32 + lane) * 16;
+                    const int vi = vr + u * 32 + lane;
+                    const int y0 = vi * 16;
                     src[u] = make_uint4(0, 0, 0, 0);
                     rs[u] = 0; re[u] = 0; kk[u] = 0;
-                    if (vb + u * 32 + lane > v_hi) continue;
-                    const int k = owner_of(slot, cnt, y0);
-                    const int64_t rk = slot[k] + PADL, ek = rk + sm[k];
-                    const int64_t a = max(y0, rk), b = min(y0 + 16, ek);
+                    if (vi >= nvec) continue;
+                    const int k = owner_of32(slot32, cnt, y0);
+                    const int rk = slot32[k] + PADL, ek = rk + sm[k];
+                    const int a = max(y0, rk), b = min(y0 + 16, ek);
                     kk[u] = k;
                     if (a < b) {
-                        rs[u] = (int)(a - y0); re[u] = (int)(b - y0);
-                        const int64_t s0 = y0 + rdelta[k];  // payload index of the vector's byte 0 (16-aligned address)
-                        if (s0 >= r0 && s0 + 16 <= rN) {  // whole block inside the caller's payload
-                            src[u] = __ldg(reinterpret_cast<const uint4*>(P.refs + s0));
+                        rs[u] = a - y0; re[u] = b - y0;
+                        if (y0 >= ylo[k] && y0 <= yhi[k]) {  // whole block inside the caller's payload
+                            src[u] = __ldg(reinterpret_cast<const uint4*>(srcb[k] + y0));
                         } else {
                             uint32_t w[4] = {0, 0, 0, 0};
-                            for (int bb = rs[u]; bb < re[u]; ++bb) w[bb >> 2] |= (uint32_t)P.refs[s0 + bb] << (8 * (bb & 3));
+                            for (int bb = rs[u]; bb < re[u]; ++bb) w[bb >> 2] |= (uint32_t)srcb[k][y0 + bb] << (8 * (bb & 3));
                             src[u] = make_uint4(w[0], w[1], w[2], w[3]);
                         }
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < PACK_FB; ++u) {
-                    if (vb + u * 32 + lane > v_hi) continue;
-                    const int64_t y0 = (vb + u * 32 + lane) * 16;
+                    const int vi = vr + u * 32 + lane;
+                    if (vi >= nvec) continue;
+                    const int y0 = vi * 16;
                     uint4 o = make_uint4(padw, padw, padw, padw);
                     if (re[u] > rs[u]) {
                         // reference bytes [rs, re) of the vector converted, the rest (and invalid
                         // symbols) pad codes
                         uint32_t c[4], nz[4];
                         conv16m(src[u], dna, lut, c, nz);
-                        const uint32_t r16 = ((1u << re[u]) - 1u) ^ ((1u << rs[u]) - 1u);
-                        uint32_t ow[4], badacc = 0;
+                        if (rs[u] == 0 && re[u] == 16 && (nz[0] | nz[1] | nz[2] | nz[3]) == 0u) {
+                            o = make_uint4(c[0], c[1], c[2], c[3]);  // interior vector, all symbols valid
+                        } else {
+                            const uint32_t r16 = ((1u << re[u]) - 1u) ^ ((1u << rs[u]) - 1u);
+                            uint32_t ow[4], badacc = 0;
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t rm = expand_nibble(r16, q);
-                            const uint32_t bb = ((nz[q] >> 7) * 0xffu) & rm;
-                            badacc |= bb;
-                            const uint32_t keep = rm & ~bb;
-                            ow[q] = (c[q] & keep) | (padw & ~keep);
+                            for (int q = 0; q < 4; ++q) {
+                                const uint32_t rm = expand_nibble(r16, q);
+                                const uint32_t bb = ((nz[q] >> 7) * 0xffu) & rm;
+                                badacc |= bb;
+                                const uint32_t keep = rm & ~bb;
+                                ow[q] = (c[q] & keep) | (padw & ~keep);
+                            }
+                            if (badacc) badbits |= 1u << kk[u];
+                            o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
                         }
-                        if (badacc) badbits |= 1u << kk[u];
-                        o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
                     }
-                    store16_within(P.rcode, y0, o, lo, hi);
+                    if (y0 >= lo_r && y0 + 16 <= hi_r) {
+                        *reinterpret_cast<uint4*>(rdst + y0) = o;
+                    } else {  // span edge: only this warp's bytes (the neighbour warp writes the others)
+                        const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                        for (int bb = 0; bb < 16; ++bb)
+                            if (y0 + bb >= lo_r && y0 + bb < hi_r) rdst[y0 + bb] = (uint8_t)(w[bb >> 2] >> (8 * (bb & 3)));
+                    }
                 }
             }
             // ---- queries: output vectors of [qlo, qhi) in qcode (no pads; shift qshift - q0) ----
@@ -312,43 +354,59 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
             const int64_t qhi = __shfl_sync(FULL, qb, cnt - 1) - q0 + qshift;
             const int64_t qd = q0 - qshift;  // payload index of code position y is y + qd
             if (qhi > qlo) {
-                const int64_t qv_hi = (qhi - 1) >> 4;
-                for (int64_t vb = qlo >> 4; vb <= qv_hi; vb += 32 * PACK_FB) {
+                // 32-bit offsets relative to the span's first 16-byte vector
+                const int64_t qbase = qlo & ~(int64_t)15;
+                const int qn = (int)(((qhi - 1) >> 4) - (qlo >> 4)) + 1;
+                const int qlo_r = (int)(qlo - qbase), qhi_r = (int)(qhi - qbase);
+                const uint8_t* qsrc = P.queries + qbase + qd;
+                uint8_t* qdst = P.qcode + qbase;
+                for (int vr = 0; vr < qn; vr += 32 * PACK_FB) {
                     uint4 src[PACK_FB];
 #pragma unroll
                     for (int u = 0; u < PACK_FB; ++u) {
-                        const int64_t y0 = (vb + u * 32 + lane) * 16;
+                        const int vi = vr + u * 32 + lane;
+                        const int y0 = vi * 16;
                         src[u] = make_uint4(0, 0, 0, 0);
-                        if (vb + u * 32 + lane > qv_hi) continue;
-                        if (y0 >= qlo && y0 + 16 <= qhi) {
-                            src[u] = __ldg(reinterpret_cast<const uint4*>(P.queries + y0 + qd));
+                        if (vi >= qn) continue;
+                        if (y0 >= qlo_r && y0 + 16 <= qhi_r) {
+                            src[u] = __ldg(reinterpret_cast<const uint4*>(qsrc + y0));
                         } else {  // span edge: only bytes inside [qlo, qhi)
                             uint32_t w[4] = {0, 0, 0, 0};
                             for (int bb = 0; bb < 16; ++bb)
-                                if (y0 + bb >= qlo && y0 + bb < qhi) w[bb >> 2] |= (uint32_t)P.queries[y0 + qd + bb] << (8 * (bb & 3));
+                                if (y0 + bb >= qlo_r && y0 + bb < qhi_r) w[bb >> 2] |= (uint32_t)qsrc[y0 + bb] << (8 * (bb & 3));
                             src[u] = make_uint4(w[0], w[1], w[2], w[3]);
                         }
                     }
 #pragma unroll
                     for (int u = 0; u < PACK_FB; ++u) {
-                        if (vb + u * 32 + lane > qv_hi) continue;
-                        const int64_t y0 = (vb + u * 32 + lane) * 16;
+                        const int vi = vr + u * 32 + lane;
+                        if (vi >= qn) continue;
+                        const int y0 = vi * 16;
                         uint32_t cw[4], nz[4];
                         conv16m(src[u], dna, lut, cw, nz);
                         if ((nz[0] | nz[1] | nz[2] | nz[3]) != 0u) {
-                        const int lo16 = qlo - y0 > 0 ? (int)(qlo - y0) : 0, hi16 = qhi - y0 < 16 ? (int)(qhi - y0) : 16;
-                        const uint32_t r16 = ((1u << hi16) - 1u) ^ ((1u << lo16) - 1u);
+                            const int lo16 = qlo_r - y0 > 0 ? qlo_r - y0 : 0, hi16 = qhi_r - y0 < 16 ? qhi_r - y0 : 16;
+                            const uint32_t r16 = ((1u << hi16) - 1u) ^ ((1u << lo16) - 1u);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t bb = ((nz[q] >> 7) * 0xffu) & expand_nibble(r16, q);
-                            if (bb) {  // rare: attribute each bad byte to its pair, store pads instead
-                                for (int b = 0; b < 4; ++b)
-                                    if ((bb >> (8 * b)) & 0xffu) badbits |= 1u << owner_of(sqa, cnt, y0 + qd + 4 * q + b);
+                            for (int q = 0; q < 4; ++q) {
+                                const uint32_t bb = ((nz[q] >> 7) * 0xffu) & expand_nibble(r16, q);
+                                if (bb) {  // rare: attribute each bad byte to its pair, store pads instead
+                                    for (int b = 0; b < 4; ++b)
+                                        if ((bb >> (8 * b)) & 0xffu)
+                                            badbits |= 1u << owner_of(sqa, cnt, qbase + y0 + qd + 4 * q + b);
+                                }
+                                cw[q] = (cw[q] & ~bb) | (padw & bb);
                             }
-                            cw[q] = (cw[q] & ~bb) | (padw & bb);
                         }
+                        const uint4 o = make_uint4(cw[0], cw[1], cw[2], cw[3]);
+                        if (y0 >= qlo_r && y0 + 16 <= qhi_r) {
+                            *reinterpret_cast<uint4*>(qdst + y0) = o;
+                        } else {  // span edge: only this warp's bytes
+                            const uint32_t w[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                            for (int bb = 0; bb < 16; ++bb)
+                                if (y0 + bb >= qlo_r && y0 + bb < qhi_r) qdst[y0 + bb] = (uint8_t)(w[bb >> 2] >> (8 * (bb & 3)));
                         }
-                        store16_within(P.qcode, y0, make_uint4(cw[0], cw[1], cw[2], cw[3]), qlo, qhi);
                     }
                 }
             }
