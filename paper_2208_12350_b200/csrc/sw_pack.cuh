@@ -115,8 +115,46 @@ __device__ __forceinline__ uint32_t dna4(uint32_t w, uint32_t& nz) {
     return c;
 }
 
+// DNA, four ASCII bytes at a time, without the invalid-byte markers: the codes and a word that is
+// zero iff all four bytes are valid letters (dna4's diff).
+__device__ __forceinline__ uint32_t dna4d(uint32_t w, uint32_t& diff) {
+    const uint32_t u = w & 0xdfdfdfdfu;
+    const uint32_t c = (u >> 1) & 0x03030303u;
+    const uint32_t t = c | (c >> 4);
+    const uint32_t sel = __byte_perm(t, 0u, 0x4420u);
+    diff = __byte_perm(0x47544341u, 0u, sel) ^ u;
+    return c;
+}
+__device__ __forceinline__ uint32_t nz_of_diff(uint32_t diff) {
+    return (((diff & 0x7f7f7f7fu) + 0x7f7f7f7fu) | diff) & 0x80808080u;
+}
+
 // Codes of 16 ASCII bytes (DNA: arithmetic, protein: table) and their invalid-byte
-// markers (0x80 per invalid byte).
+// markers (0x80 per invalid byte).  Returns true when every byte is valid (the markers are then 0).
+__device__ __forceinline__ bool conv16v(const uint4 v, bool dna, const uint8_t* lut, uint32_t (&c)[4], uint32_t (&nz)[4]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    if (dna) {
+        uint32_t d[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[q] = dna4d(w[q], d[q]);
+        if ((d[0] | d[1] | d[2] | d[3]) == 0u) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) nz[q] = 0u;
+            return true;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nz[q] = nz_of_diff(d[q]);
+        return false;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t bm = 0;
+        c[q] = conv4(w[q], lut, bm);
+        nz[q] = c[q] & 0x80808080u;
+    }
+    return (nz[0] | nz[1] | nz[2] | nz[3]) == 0u;
+}
+
 __device__ __forceinline__ void conv16m(const uint4 v, bool dna, const uint8_t* lut, uint32_t (&c)[4], uint32_t (&nz)[4]) {
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -321,8 +359,8 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
                         // reference bytes [rs, re) of the vector converted, the rest (and invalid
                         // symbols) pad codes
                         uint32_t c[4], nz[4];
-                        conv16m(src[u], dna, lut, c, nz);
-                        if (rs[u] == 0 && re[u] == 16 && (nz[0] | nz[1] | nz[2] | nz[3]) == 0u) {
+                        const bool allv = conv16v(src[u], dna, lut, c, nz);
+                        if (rs[u] == 0 && re[u] == 16 && allv) {
                             o = make_uint4(c[0], c[1], c[2], c[3]);  // interior vector, all symbols valid
                         } else {
                             const uint32_t r16 = ((1u << re[u]) - 1u) ^ ((1u << rs[u]) - 1u);
@@ -383,8 +421,7 @@ __global__ void __launch_bounds__(256, SW_PACK_MINB) pack_kernel(PackParams P) {
                         if (vi >= qn) continue;
                         const int y0 = vi * 16;
                         uint32_t cw[4], nz[4];
-                        conv16m(src[u], dna, lut, cw, nz);
-                        if ((nz[0] | nz[1] | nz[2] | nz[3]) != 0u) {
+                        if (!conv16v(src[u], dna, lut, cw, nz)) {
                             const int lo16 = qlo_r - y0 > 0 ? qlo_r - y0 : 0, hi16 = qhi_r - y0 < 16 ? qhi_r - y0 : 16;
                             const uint32_t r16 = ((1u << hi16) - 1u) ^ ((1u << lo16) - 1u);
 #pragma unroll
