@@ -212,13 +212,13 @@ __device__ __forceinline__ void store16_within(uint8_t* dst, int64_t y0, uint4 v
 }
 
 #ifndef SW_PACK_PPW
-#define SW_PACK_PPW 8
+#define SW_PACK_PPW 16
 #endif
 #ifndef SW_PACK_FB
-#define SW_PACK_FB 4
+#define SW_PACK_FB 2
 #endif
 #ifndef SW_PACK_MINB
-#define SW_PACK_MINB 3
+#define SW_PACK_MINB 4
 #endif
 constexpr int PACK_WARPS = 8;  // warps per pack block (256 threads)
 constexpr int PACK_PPW = SW_PACK_PPW;    // pairs per warp
