@@ -55,12 +55,15 @@ __device__ __forceinline__ void decode_key(unsigned long long key, int& S, int& 
 #define SW_FIN_PPW 8
 #endif
 #ifndef SW_FIN_FB
-#define SW_FIN_FB 4
+#define SW_FIN_FB 2
+#endif
+#ifndef SW_FIN_MINB
+#define SW_FIN_MINB 1
 #endif
 constexpr int FIN_PPW = SW_FIN_PPW;
 constexpr int FIN_FB = SW_FIN_FB;   // words per lane loaded before any is stored
 
-__global__ void __launch_bounds__(256) finish_fwd_kernel(FinishParams P) {
+__global__ void __launch_bounds__(256, SW_FIN_MINB) finish_fwd_kernel(FinishParams P) {
     __shared__ int s_route[N_ROUTES];
     __shared__ int s_band[N_BAND];
     if (batch_rejected(P.stats)) {  // whole batch invalid (malformed / beyond the reservation): every field -1
