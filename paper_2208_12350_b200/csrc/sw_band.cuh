@@ -110,8 +110,12 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 #define SW_BAND_CHECK 0  // development builds: trap on a read outside the pair's qrev slot / rrev region
 #endif
 
+#ifndef SW_BAND_MINB
+#define SW_BAND_MINB 2  // 4-warp blocks per SM: 2 (163 registers, more of the 8-cell step in flight) measured faster than 3 or 4
+#endif
+
 template <int W>
-__global__ void __launch_bounds__(128, 4) band_rev_kernel(BandParams P) {
+__global__ void __launch_bounds__(128, SW_BAND_MINB) band_rev_kernel(BandParams P) {
     using T = TS16;
     constexpr int K = BAND_K, KH = BAND_KH;
     constexpr int SEGS = 32 / W, SLOTS = 2 * SEGS, CAP = W * K;
