@@ -59,6 +59,9 @@
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4
 #endif
+#ifndef SW_MIN_BLOCKS_REV
+#define SW_MIN_BLOCKS_REV SW_MIN_BLOCKS  // reverse-pass kernels (DNA / int32 geometry)
+#endif
 #ifndef SW_BODY_BLOCKS
 #define SW_BODY_BLOCKS 2   // 4-column blocks per unrolled loop body (forward; chosen by tools/gevo_search.py)
 #endif
@@ -963,7 +966,7 @@ __device__ __forceinline__ int sweep_skew2(const WaveParams& P, const uint8_t* p
 }
 
 template <class T, int W, int K, bool REV, bool TAG, bool LIN>
-__global__ void __launch_bounds__((K == SW_KP && W == SW_WP) ? SW_PROT_THREADS : 128, (K == SW_KP && W == SW_WP) ? SW_PROT_BLOCKS : SW_MIN_BLOCKS)
+__global__ void __launch_bounds__((K == SW_KP && W == SW_WP) ? SW_PROT_THREADS : 128, (K == SW_KP && W == SW_WP) ? SW_PROT_BLOCKS : REV ? SW_MIN_BLOCKS_REV : SW_MIN_BLOCKS)
     wavefront_kernel(const WaveParams P) {
     constexpr bool IMK = SW_IMERGE && SW_TAG_LAZY && TAG && !REV && T::NH == 2 && K == 10;
     using G = Geometry<W, K, T, IMK>;
