@@ -55,7 +55,7 @@ __device__ __forceinline__ void decode_key(unsigned long long key, int& S, int& 
 #define SW_FIN_PPW 8
 #endif
 #ifndef SW_FIN_FB
-#define SW_FIN_FB 2
+#define SW_FIN_FB 4
 #endif
 #ifndef SW_FIN_MINB
 #define SW_FIN_MINB 1
