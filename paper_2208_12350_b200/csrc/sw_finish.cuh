@@ -57,6 +57,9 @@ __device__ __forceinline__ void decode_key(unsigned long long key, int& S, int& 
 #ifndef SW_FIN_FB
 #define SW_FIN_FB 4
 #endif
+#ifndef SW_REV_KEY_N2
+#define SW_REV_KEY_N2 0  // 1: single-stripe reverse items grouped by n2 (the span proxy) instead of S
+#endif
 #ifndef SW_FIN_MINB
 #define SW_FIN_MINB 1
 #endif
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(256, SW_FIN_MINB) finish_fwd_kernel(FinishPara
                 // length (no narrow band) can outweigh a higher-identity pair with more stripes
                 const int B = (S + P.max_sigma - 1) / P.max_sigma;
                 const int bcols = max(1, (int)min((long long)m2, (long long)n2 + m2 - 2LL * B + rows));
-                const uint32_t key = stripes == 1 ? work_key(route, 1u, (uint32_t)S)
+                const uint32_t key = stripes == 1 ? work_key(route, 1u, (uint32_t)(SW_REV_KEY_N2 ? n2 : S))
                                    : P.rev_small ? work_key(route, stripes, (uint32_t)bcols)
                                    : work_key(route, (uint32_t)min(0x3fffLL, ((long long)stripes * bcols) >> 8) + 1u, (uint32_t)bcols);
                 rp = P.rpos[p];

@@ -113,7 +113,7 @@
 #define SW_UNROLL 4
 #endif
 #ifndef SW_ABLATE
-#define SW_ABLATE 0        // timing experiments only (1: no improvement path, 2: no PRMT)
+#define SW_ABLATE 0        // timing experiments only (1: no improvement path, 2: no PRMT, 4: no stripe hand-off)
 #endif
 #ifndef SW_SINGLE_ONLY
 #define SW_SINGLE_ONLY 0   // experiment: compile only the single-stripe sweep
@@ -578,7 +578,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
             if (MULTI) {
                 bHO = bnd[u].x * useL0 + bconst;  // IMAD (FMA pipe)
                 bF = bnd[u].y * useL0;
-                bnd[u] = __ldcg(scr_in + t + U);
+                if (!(SW_ABLATE & 4)) bnd[u] = __ldcg(scr_in + t + U);  // (ablation 4: timing only, no hand-off)
             }
             // row above: neighbour lane's last row at this column, or the stripe boundary (lane 0)
             const uint32_t upHO = __shfl_up_sync(FULL, hoLast, 1, W) * notL0 + bHO;
@@ -772,7 +772,7 @@ __device__ __forceinline__ int sweep(const WaveParams& P, const uint8_t* prof, v
                 next_ev = ev[0];
                 if (NH == 2) next_ev = min(next_ev, ev[NH - 1]);
             }
-            if (st_lane) scr_out[t - (W - 1)] = make_uint2(hoLast, fLast);
+            if (st_lane && !(SW_ABLATE & 4)) scr_out[t - (W - 1)] = make_uint2(hoLast, fLast);
         }
         if (TAG && !PT && !REV && (SW_TAG_LAZY || nbt != best)) tag_commit(nbt, t0);
         if (TAG && REV) {
