@@ -1004,3 +1004,45 @@ def test_banded_reverse_matches_row_sweep(kind):
             assert_parity(a.align(b), exp, b)  # default mode (row sweep for batches this small)
     finally:
         a.close()
+
+
+def test_banded_reverse_edges():
+    """Banded reverse kernels at their routing edges (sw_band.cuh, finish_fwd): reversed query prefixes of
+    1, 175-177 rows (BAND_MAX_N2 = 176), bands of exactly 32 / 33 / 64 / 65 diagonals (one deletion run
+    sized so DI + DD + 1 lands on the edge), references shorter than the query, ends in the first
+    columns, identical sequences (DI = DD = 0) and odd pair counts (empty halves), on a poisoned handle with
+    the band kernels forced; all five fields vs the oracle."""
+    rng = np.random.default_rng(61)
+    A = list("ACGT")
+    sc = {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -6, "gap_extend": -1}
+    pairs = []
+    for n in (1, 2, 7, 150, 170):
+        x = "".join(rng.choice(A, n))
+        pairs.append((x, x))                                              # identical
+        pairs.append((x, x[: max(1, n // 3)]))                            # reference shorter than the query
+        pairs.append((x, x + "".join(rng.choice(A, 300))))                # end in the first columns
+    for n in (175, 176, 177):                                             # n2 around BAND_MAX_N2 = 176 (max_s n2 <= 511)
+        x = "".join(rng.choice(A, n))
+        pairs.append((x, "".join(rng.choice(A, 50)) + x + "".join(rng.choice(A, 50))))
+    for k in range(1, 70, 3):                                             # one deletion run of k: DD grows with k
+        x = rng.choice(A, 150)
+        c = int(rng.integers(20, 130))
+        r = np.concatenate([rng.choice(A, int(rng.integers(0, 40))), x[:c], rng.choice(A, k), x[c:],
+                            rng.choice(A, int(rng.integers(0, 40)))])
+        pairs.append(("".join(x), "".join(r)))
+    for k in range(1, 12):                                                # insertion runs: DI grows with k
+        x = rng.choice(A, 150)
+        c = int(rng.integers(20, 130))
+        q = np.concatenate([x[:c], rng.choice(A, k), x[c:]])
+        pairs.append(("".join(q), "".join(rng.choice(A, 30)) + "".join(x)))
+    pairs = pairs[: len(pairs) - (1 - len(pairs) % 2)]                   # an odd count: a half stays empty
+    b = synth.from_pairs(pairs, sc)
+    exp = oracle_batch(b)
+    a = sw.Aligner(0, poison=True)
+    try:
+        for mode in (sw.SW_MODE_BAND_ALWAYS, sw.SW_MODE_NO_BAND):
+            a.set_mode(mode)
+            assert_parity(a.align(b), exp, b)
+            assert a.batch_status()[0] == sw.SW_OK
+    finally:
+        a.close()
