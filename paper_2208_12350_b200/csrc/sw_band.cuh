@@ -67,11 +67,17 @@ __host__ __device__ __forceinline__ int band_dlo(int DI) { return -((DI + BAND_D
 __host__ __device__ __forceinline__ int band_jw(int n2, int cap) { return (n2 + cap + BAND_JPAD + 3) & ~3; }
 static_assert(BAND_ROFF + ((BAND_MAX_N2 + 64 + BAND_JPAD + 3) & ~3) <= BAND_SLOT, "band slot holds the selectors");
 
-// Tags of a lane's 4-step block: cell k of step u sits at (j', i') = (J + k + ceil(u/2), I - k + floor(u/2));
-// tag = 63 - rank of (j', i') among the block's 32 cells (the running max picks the lexmin).
+// Tags of a lane's BAND_BLK-step block: cell k of step u sits at (j', i') = (J + k + ceil(u/2), I - k + floor(u/2));
+// tag = 63 - rank of (j', i') among the block's 8 BAND_BLK cells (the running max picks the lexmin; the
+// pairs (j', i') are distinct: their sum fixes u).  8 steps = 64 cells fill the 6 tag bits.
+#ifndef SW_BAND_BLK
+#define SW_BAND_BLK 4
+#endif
+constexpr int BAND_BLK = SW_BAND_BLK;
+static_assert(BAND_BLK == 4 || BAND_BLK == 8, "band tag block: 4 or 8 steps");
 __host__ __device__ constexpr int band_tag(int u, int k) {
     int rank = 0;
-    for (int u2 = 0; u2 < 4; ++u2)
+    for (int u2 = 0; u2 < BAND_BLK; ++u2)
         for (int k2 = 0; k2 < BAND_KH; ++k2) {
             const int jo = k + (u + 1) / 2, io = u / 2 - k, jo2 = k2 + (u2 + 1) / 2, io2 = u2 / 2 - k2;
             if (jo2 < jo || (jo2 == jo && io2 < io)) ++rank;
@@ -141,6 +147,11 @@ __global__ void __launch_bounds__(128, SW_BAND_MINB) band_rev_kernel(BandParams 
     const uint32_t o2s = T::splat(o), e2 = T::splat(P.sc.gap_extend);
     const uint32_t qtab = (uint32_t)__cvta_generic_to_shared(s_qprof);
     const uint32_t tag_mul = P.tag_mul;
+#ifndef SW_BAND_QIMAD
+#define SW_BAND_QIMAD 0
+#endif
+    // (SW_BAND_QIMAD) opaque shift multipliers so the byte extraction stays IMAD + IMAD.HI
+    const uint32_t shl_c[4] = {opaque(1u << 24), opaque(1u << 16), opaque(1u << 8), opaque(1u)};
     // neighbours across lanes: lane L-1's last slot (left of slot 0), lane L+1's first (above slot K-1);
     // the band's own edges take the border (R = H + o = o, E = F = 0) by multiply-add (FMA pipe)
     const uint32_t notFirst = opaque(L != 0 ? 1u : 0u), notLast = opaque(L != W - 1 ? 1u : 0u);
@@ -248,8 +259,14 @@ __global__ void __launch_bounds__(128, SW_BAND_MINB) band_rev_kernel(BandParams 
                 if ((u & 1) == 0) {
                     // query shift: q'[8b - 8L + u/2] into ring slot u/2
                     const int e = u >> 1;
+#if SW_BAND_QIMAD
+                    // byte e & 3 of the word by multiply-high (FMA pipe): (w * 2^(24 - 8b)) mod 2^32, then >> 24
+                    const uint32_t ca = __umulhi(qw[0][e >> 2] * shl_c[e & 3], 256u);
+                    const uint32_t cb = __umulhi(qw[1][e >> 2] * shl_c[e & 3], 256u);
+#else
                     const uint32_t ca = prmt(qw[0][e >> 2], 0u, (uint32_t)(0x4440 | (e & 3)));
                     const uint32_t cb = prmt(qw[1][e >> 2], 0u, (uint32_t)(0x4440 | (e & 3)));
+#endif
                     if (SW_BAND_CHECK && (ca > 7u || cb > 7u)) { printf("band code %u %u\n", ca, cb); __trap(); }
                     QA[e] = lds32(qtab + ca * 4u);
                     QB[e] = lds32(qtab + cb * 4u);
@@ -288,15 +305,15 @@ __global__ void __launch_bounds__(128, SW_BAND_MINB) band_rev_kernel(BandParams 
                     F[s] = T::addmax_relu(uF, e2, uR);                        // F^ = max(F^ + e, H + o, 0), cell above
                     const uint32_t X = T::addmax(R[s], sc, E[s]);             // max(H_diag + s, E^)
                     R[s] = T::addmax(F[s], o2s, T::add(X, o2s));              // H + o = max(F^, X) + o
-                    Xt[k] = X * tag_mul + (uint32_t)band_tag(u & 3, k) * 0x10001u;
+                    Xt[k] = X * tag_mul + (uint32_t)band_tag(u & (BAND_BLK - 1), k) * 0x10001u;
                 }
 #pragma unroll
                 for (int k = 0; k < KH; k += 2) nbt = T::max3(nbt, Xt[k], Xt[k + 1]);
-                if ((u & 3) == 3) {
+                if ((u & (BAND_BLK - 1)) == BAND_BLK - 1) {
                     // block check: some half's maximum reached S * 64 (every in-band cell holds <= S)
                     const uint32_t x = T::max2(nbt, tgt64) ^ nbt;
                     if (((x - 0x00010001u) & ~x & 0x80008000u) != 0u) {
-                        const int ub = u - 3;
+                        const int ub = u - (BAND_BLK - 1);
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
                             const int v = T::get(nbt, h);
@@ -304,7 +321,7 @@ __global__ void __launch_bounds__(128, SW_BAND_MINB) band_rev_kernel(BandParams 
                                 const int tag = v & 63;
                                 int cu = 0, ck = 0;
 #pragma unroll
-                                for (int uu = 0; uu < 4; ++uu)
+                                for (int uu = 0; uu < BAND_BLK; ++uu)
 #pragma unroll
                                     for (int kk = 0; kk < KH; ++kk)
                                         if (band_tag(uu, kk) == tag) { cu = uu; ck = kk; }

@@ -1,0 +1,13 @@
+#!/bin/bash
+# A/B of band-kernel variants: banded parity tests per library, then c4 / c2 timings (gpurun_out/r09/$1)
+set -u
+LOG=$1; shift
+mkdir -p gpurun_out/r09
+for lib in "$@"; do
+  echo "lib $lib" >> gpurun_out/r09/$LOG
+  SW_B200_LIB=$lib timeout 600 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "banded or gap_band" 2>&1 | tail -1 >> gpurun_out/r09/$LOG
+done
+for cfg in c4 c2; do for lib in "$@"; do
+  SW_B200_LIB=$lib timeout 600 python tools/quick_time.py $cfg >> gpurun_out/r09/$LOG 2>&1
+done; done
+grep -E "^lib|passed|failed|stages|lib:" gpurun_out/r09/$LOG
