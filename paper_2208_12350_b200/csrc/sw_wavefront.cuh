@@ -52,9 +52,12 @@
 #define SW_CODE4 0         // 1 (measurement variant): DNA TAG forward reads 4-bit reference codes, 8 per word
 #endif
 #ifndef SW_COOP_STRIPES
-#define SW_COOP_STRIPES 8  // reverse items with at least this many stripes are swept by all warps of a CTA
+#define SW_COOP_STRIPES 16 // reverse items with at least this many stripes are swept by all warps of a CTA (A/B 4-32: 16 best after the gap-aware band)
 #endif
-#define COOP_PUBLISH 32    // a cooperative producer publishes its hand-off progress every 32 column steps
+#ifndef SW_COOP_PUBLISH
+#define SW_COOP_PUBLISH 32
+#endif
+#define COOP_PUBLISH SW_COOP_PUBLISH  // a cooperative producer publishes its hand-off progress every COOP_PUBLISH column steps
 
 #ifndef SW_MIN_BLOCKS
 #define SW_MIN_BLOCKS 4

@@ -852,19 +852,20 @@ def test_reverse_band_multistripe(aligner, kind):
 
 @pytest.mark.parametrize("kind", ["dna_mixed", "dna_cheap_gaps", "protein"])
 def test_reverse_cooperative_items(aligner, kind):
-    """Reverse items with >= SW_COOP_STRIPES stripes are swept by all warps of a CTA, consecutive
+    """Reverse items with >= SW_COOP_STRIPES (16) stripes are swept by all warps of a CTA, consecutive
     stripes on consecutive warps with published hand-off progress (sw_wavefront.cuh).  Long pairs
-    (8-20 stripes) of mixed identity -- unrelated pairs whose start lies far from the origin (cheap
+    (16-24 stripes) of mixed identity -- unrelated pairs whose start lies far from the origin (cheap
     gaps make their gapped score grow with length), high-identity ones, tandem repeats -- plus short
     partners in the same items; all five fields vs the oracle."""
     rng = np.random.default_rng({"dna_mixed": 41, "dna_cheap_gaps": 42, "protein": 43}[kind])
+    # lengths from just above SW_COOP_STRIPES (16) stripes: 128-row protein / 160-row DNA stripes
     if kind == "protein":
-        alpha, sc, lo, hi = list("ARNDCQEGHILKMFPSTWYV"), synth.PROTEIN_SCORING, 1030, 1900
+        alpha, sc, lo, hi = list("ARNDCQEGHILKMFPSTWYV"), synth.PROTEIN_SCORING, 2050, 2700
     elif kind == "dna_cheap_gaps":
-        alpha, lo, hi = list("ACGT"), 1290, 2600
+        alpha, lo, hi = list("ACGT"), 2570, 3300
         sc = {"alphabet": "dna", "match": 3, "mismatch": -3, "gap_open": -6, "gap_extend": -1}
     else:
-        alpha, lo, hi = list("ACGT"), 1290, 3200
+        alpha, lo, hi = list("ACGT"), 2570, 3800
         sc = {"alphabet": "dna", "match": 2, "mismatch": -3, "gap_open": -5, "gap_extend": -2}
     pairs = []
     for k in range(14):
