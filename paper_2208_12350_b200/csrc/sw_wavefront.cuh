@@ -99,7 +99,7 @@
 #define SW_PRED_IMPROVE 0     // non-TAG forward: record running-max improvements branch-free
 #endif
 #ifndef SW_REV_BODY_BLOCKS
-#define SW_REV_BODY_BLOCKS 1  // reverse pass: the stop column is re-checked after every block either way
+#define SW_REV_BODY_BLOCKS 2  // reverse pass: the stop column is re-checked after every block either way (2 vs 1: c3 reverse 2.78 vs 2.94 ms, c4 8.75 vs 8.83, c5 47.6 vs 46.2)
 #endif
 // Launch bounds of the 8-row (protein) geometry: 3-warp blocks, 5 per SM by shared memory, so
 // up to 136 registers per thread keep all 15 warps resident.
